@@ -1,0 +1,349 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle for the DCDS hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Single-threaded C99, no intrinsics, no
+ * blocking, fusion or reordering beyond what the paper's algorithm states.  Shares no code
+ * with the CUDA path.
+ *
+ * Each function cites the passage it follows (P:n = PAPER.md line n).  Readings of points
+ * where the paper is silent are the DESIGN.md / SURVEY.md 8(c) ledger entries C1..C22.
+ *
+ * Parity pins (tests/test_oracle_*.py) tie this file to the paper:
+ *   - Table VII DCDS block, 64 published integers, through oracle_dcds_cost
+ *     with the Euclidean cost of P:301 AND through the pixel SAD path (oracle_dcds) on
+ *     frames whose SAD surface is B*|q-t|^2 + K;
+ *   - P:297 (7 points for a zero MV; 10 or 11 for (+-1,0)/(0,+-1)), Eq. 8 branches
+ *     and the Fig. 6 example MV (1,3);
+ *   - Table VIII distribution 2, Table II weighted by the NSP map;
+ *   - FS against an independent numpy brute force; zero-noise translations (closed form);
+ *   - PSNR closed forms.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------------ */
+/* Reference pixel with edge replication (reading C9: H.263-style unrestricted MV).      */
+/* ------------------------------------------------------------------------------------ */
+static int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+static int R(const uint8_t* ref, int W, int H, int x, int y) {
+    return ref[(long)clampi(y, 0, H - 1) * W + clampi(x, 0, W - 1)];
+}
+
+static int check_frame(int W, int H, int B) {
+    if (W <= 0 || H <= 0 || B <= 0) return -1;
+    if (W % B != 0 || H % B != 0) return -1;
+    return 0;
+}
+
+/* SAD(q) = sum_{i,j<B} |cur(by+i, bx+j) - R(bx+dx+j, by+dy+i)|   (MAD * B^2). */
+static uint32_t sad_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int B,
+                          int bx, int by, int dx, int dy) {
+    uint32_t s = 0;
+    for (int i = 0; i < B; i++) {
+        for (int j = 0; j < B; j++) {
+            int c = cur[(long)(by + i) * W + (bx + j)];
+            int r = R(ref, W, H, bx + dx + j, by + dy + i);
+            s += (uint32_t)(c > r ? c - r : r - c);
+        }
+    }
+    return s;
+}
+
+int oracle_sad(const uint8_t* cur, const uint8_t* ref, int W, int H, int B,
+               int bx, int by, int dx, int dy, uint32_t* sad_out) {
+    if (check_frame(W, H, B) || !cur || !ref || !sad_out) return -1;
+    if (bx < 0 || by < 0 || bx + B > W || by + B > H) return -1;
+    *sad_out = sad_block(cur, ref, W, H, B, bx, by, dx, dy);
+    return 0;
+}
+
+static uint64_t sse_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int B,
+                          int bx, int by, int dx, int dy) {
+    uint64_t s = 0;
+    for (int i = 0; i < B; i++) {
+        for (int j = 0; j < B; j++) {
+            int d = (int)cur[(long)(by + i) * W + (bx + j)] - R(ref, W, H, bx + dx + j, by + dy + i);
+            s += (uint64_t)(d * d);
+        }
+    }
+    return s;
+}
+
+int oracle_sse_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int B,
+                     int bx, int by, int dx, int dy, uint64_t* sse_out) {
+    if (check_frame(W, H, B) || !cur || !ref || !sse_out) return -1;
+    if (bx < 0 || by < 0 || bx + B > W || by + B > H) return -1;
+    *sse_out = sse_block(cur, ref, W, H, B, bx, by, dx, dy);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* DCDS search with an abstract cost.                                        */
+/* ------------------------------------------------------------------------------------ */
+
+/* Patterns, in the fixed order of reading C7 (centre first, then ascending
+ * (|dy|,|dx|,dy,dx)).  Geometry: readings C1/C2.              */
+static const int HCSP[6][2] = {{-1, 0}, {1, 0}, {-2, 0}, {2, 0}, {0, -1}, {0, 1}};
+/* HDSP: distant points (+-2,0) on the horizontal long wing, near points (0,+-1).     */
+static const int HDSP[4][2] = {{-2, 0}, {2, 0}, {0, -1}, {0, 1}};
+/* VDSP: distant points (0,+-2) on the vertical long wing, near points (+-1,0).       */
+static const int VDSP[4][2] = {{-1, 0}, {1, 0}, {0, -2}, {0, 2}};
+/* Middle points: distance 1 on the long wing.                                */
+static const int HMID[2][2] = {{-1, 0}, {1, 0}};
+static const int VMID[2][2] = {{0, -1}, {0, 1}};
+
+enum { KIND_HCSP = 0, KIND_HDSP = 1, KIND_VDSP = 2, KIND_MID = 3 };
+
+typedef double (*cost_fn)(int dx, int dy, void* ctx);
+
+typedef struct {
+    int p;
+    int side;            /* 2p+1 */
+    unsigned char* seen; /* visited set V over the window (reading C5)  */
+    double* memo;        /* cost of every visited point (used by DCDS^S only) */
+    int points;          /* NSP: number of distinct feasible candidates scored */
+    cost_fn cost;
+    void* ctx;
+    int* trace;
+    int trace_cap;
+    int trace_len;
+} search_t;
+
+/* score(q): skip if infeasible (outside +-p, reading C8) or already visited (reading C5);
+ * otherwise insert into V, count it, and return its cost.  Returns 0 when skipped. */
+static int score(search_t* s, int dx, int dy, int step, int kind, double* v) {
+    if (dx < -s->p || dx > s->p || dy < -s->p || dy > s->p) return 0;
+    int idx = (dy + s->p) * s->side + (dx + s->p);
+    if (s->seen[idx]) return 0;
+    s->seen[idx] = 1;
+    s->points++;
+    *v = s->cost(dx, dy, s->ctx);
+    s->memo[idx] = *v;
+    if (s->trace && s->trace_len < s->trace_cap) {
+        int* t = s->trace + 4 * s->trace_len;
+        t[0] = step; t[1] = dx; t[2] = dy; t[3] = kind;
+    }
+    if (s->trace) s->trace_len++;
+    return 1;
+}
+
+/* scan(c, O, incumbent): score every c+o in the listed order; a new point replaces the
+ * incumbent only when strictly cheaper (reading C6).  */
+static void scan(search_t* s, int cx, int cy, const int (*off)[2], int n, int step, int kind,
+                 int* bx, int* by, double* bs) {
+    for (int k = 0; k < n; k++) {
+        double v;
+        int qx = cx + off[k][0], qy = cy + off[k][1];
+        if (score(s, qx, qy, step, kind, &v) && v < *bs) {
+            *bx = qx; *by = qy; *bs = v;
+        }
+    }
+}
+
+static int visited(const search_t* s, int dx, int dy) {
+    if (dx < -s->p || dx > s->p || dy < -s->p || dy > s->p) return 0;
+    return s->seen[(dy + s->p) * s->side + (dx + s->p)];
+}
+
+/* One DCDS search; variant 1 = DCDS^S (reading C22). */
+static void dcds_search(search_t* s, int variant, int* mvx, int* mvy, double* best) {
+    memset(s->seen, 0, (size_t)s->side * s->side);
+    s->points = 0;
+    s->trace_len = 0;
+
+    /* Step 1: HCSP centred at the origin of the search window.  The centre is the
+     * first point scored and is the incumbent. */
+    double s0;
+    score(s, 0, 0, 0, KIND_HCSP, &s0);  /* (0,0) is always feasible */
+    int bx = 0, by = 0;
+    double bs = s0;
+    scan(s, 0, 0, HCSP, 6, 0, KIND_HCSP, &bx, &by, &bs);
+    if (bx == 0 && by == 0) {  /* halfway stop */
+        *mvx = 0; *mvy = 0; *best = bs;
+        return;
+    }
+
+    /* Step 2 with switching strategy one: BMP in the horizontal
+     * direction (dy == 0, reading C3) -> HDSP, otherwise VDSP. */
+    int kind = (by == 0) ? KIND_HDSP : KIND_VDSP;
+    int cx = bx, cy = by;
+    int step = 1;  /* pass index: 0 = Step 1, 1 = Step 2, 2.. = Step 3 passes */
+    for (;;) {
+        /* Step 2 / Step 3: put the CSP centre on the current BMP and
+         * score its points. */
+        if (kind == KIND_HDSP)
+            scan(s, cx, cy, HDSP, 4, step, kind, &bx, &by, &bs);
+        else
+            scan(s, cx, cy, VDSP, 4, step, kind, &bx, &by, &bs);
+        if (bx == cx && by == cy) break;  /* BMP at the centre -> Step 4 */
+        /* Switching strategy two: near point (L1 distance 1) -> the other DDSP;
+         * distant point (distance 2) -> keep (reading C4).  Repeat (no cap, C11). */
+        int l1 = abs(bx - cx) + abs(by - cy);
+        if (l1 == 1) kind = (kind == KIND_HDSP) ? KIND_VDSP : KIND_HDSP;
+        cx = bx; cy = by;
+        step++;
+    }
+    step++;  /* Step 4 pass */
+
+    /* Step 4: identify the BMP among the two middle points and the centre
+     * (reading C10). */
+    const int (*mid)[2] = (kind == KIND_HDSP) ? HMID : VMID;
+    if (variant == 0) {
+        scan(s, cx, cy, mid, 2, step, KIND_MID, &bx, &by, &bs);
+    } else {
+        /* DCDS^S: only the middle point on the side of the cheaper distant point.
+         * Distant points are the long-wing points at distance 2; an infeasible one costs
+         * +inf; ties pick the negative side (reading C22). */
+        double dn = INFINITY, dp = INFINITY;
+        int ax = (kind == KIND_HDSP) ? 2 : 0, ay = (kind == KIND_HDSP) ? 0 : 2;
+        if (visited(s, cx - ax, cy - ay)) dn = s->memo[(cy - ay + s->p) * s->side + (cx - ax + s->p)];
+        if (visited(s, cx + ax, cy + ay)) dp = s->memo[(cy + ay + s->p) * s->side + (cx + ax + s->p)];
+        const int (*one)[2] = (dp < dn) ? mid + 1 : mid;
+        scan(s, cx, cy, one, 1, step, KIND_MID, &bx, &by, &bs);
+    }
+    *mvx = bx; *mvy = by; *best = bs;
+}
+
+static int search_init(search_t* s, int p) {
+    s->p = p;
+    s->side = 2 * p + 1;
+    s->seen = (unsigned char*)calloc((size_t)s->side * s->side, 1);
+    s->memo = (double*)calloc((size_t)s->side * s->side, sizeof(double));
+    s->trace = NULL; s->trace_cap = 0; s->trace_len = 0;
+    return (s->seen && s->memo) ? 0 : -1;
+}
+
+static void search_free(search_t* s) { free(s->seen); free(s->memo); }
+
+/* ------------------------------------------------------------------------------------ */
+/* Pixel cost: SAD of one block.                                                 */
+/* ------------------------------------------------------------------------------------ */
+typedef struct {
+    const uint8_t* cur; const uint8_t* ref; int W, H, B, bx, by;
+} pix_ctx;
+
+static double pix_cost(int dx, int dy, void* ctx) {
+    pix_ctx* c = (pix_ctx*)ctx;
+    return (double)sad_block(c->cur, c->ref, c->W, c->H, c->B, c->bx, c->by, dx, dy);
+}
+
+int oracle_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
+                int variant, int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out) {
+    if (check_frame(W, H, B) || p < 1 || !cur || !ref) return -1;
+    if (variant != 0 && variant != 1) return -1;
+    search_t s;
+    if (search_init(&s, p)) return -1;
+    pix_ctx c = {cur, ref, W, H, B, 0, 0};
+    s.cost = pix_cost; s.ctx = &c;
+    int nbx = W / B, nby = H / B;
+    for (int i = 0; i < nbx * nby; i++) {  /* raster order */
+        c.bx = (i % nbx) * B; c.by = (i / nbx) * B;
+        int mx, my; double best;
+        dcds_search(&s, variant, &mx, &my, &best);
+        if (mv_out) { mv_out[2 * i] = (int16_t)mx; mv_out[2 * i + 1] = (int16_t)my; }
+        if (sad_out) sad_out[i] = (uint32_t)best;
+        if (points_out) points_out[i] = (uint16_t)s.points;
+    }
+    search_free(&s);
+    return 0;
+}
+
+int oracle_dcds_cost(oracle_cost_fn cost, void* ctx, int p, int variant,
+                     int* mv_dx, int* mv_dy, double* cost_out, int* points_out,
+                     int* trace, int trace_cap, int* trace_len) {
+    if (!cost || p < 1 || (variant != 0 && variant != 1)) return -1;
+    search_t s;
+    if (search_init(&s, p)) return -1;
+    s.cost = cost; s.ctx = ctx;
+    s.trace = trace; s.trace_cap = trace ? trace_cap : 0;
+    int mx, my; double best;
+    dcds_search(&s, variant, &mx, &my, &best);
+    if (mv_dx) *mv_dx = mx;
+    if (mv_dy) *mv_dy = my;
+    if (cost_out) *cost_out = best;
+    if (points_out) *points_out = s.points;
+    if (trace_len) *trace_len = s.trace_len;
+    search_free(&s);
+    return 0;
+}
+
+/* Ideal unimodal surface: cost of P is its Euclidean distance to the true MV. */
+typedef struct { int tx, ty; } ideal_ctx;
+static double ideal_cost(int dx, int dy, void* ctx) {
+    ideal_ctx* t = (ideal_ctx*)ctx;
+    double ex = dx - t->tx, ey = dy - t->ty;
+    return sqrt(ex * ex + ey * ey);
+}
+
+int oracle_ideal_nsp_map(int p, int variant, int* nsp_out, int* mvx_out, int* mvy_out) {
+    if (p < 1 || !nsp_out) return -1;
+    int side = 2 * p + 1;
+    for (int ty = -p; ty <= p; ty++) {
+        for (int tx = -p; tx <= p; tx++) {
+            ideal_ctx t = {tx, ty};
+            int mx, my, pts; double c;
+            if (oracle_dcds_cost(ideal_cost, &t, p, variant, &mx, &my, &c, &pts, NULL, 0, NULL))
+                return -1;
+            int k = (ty + p) * side + (tx + p);
+            nsp_out[k] = pts;
+            if (mvx_out) mvx_out[k] = mx;
+            if (mvy_out) mvy_out[k] = my;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Full search: every candidate of the window; the brute-force quality reference. */
+/* ------------------------------------------------------------------------------------ */
+int oracle_fullsearch(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
+                      int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out) {
+    if (check_frame(W, H, B) || p < 1 || !cur || !ref) return -1;
+    int nbx = W / B, nby = H / B;
+    for (int i = 0; i < nbx * nby; i++) {
+        int bx = (i % nbx) * B, by = (i / nbx) * B;
+        /* (0,0) first (reading C13), then raster order; strict minimum. */
+        uint32_t best = sad_block(cur, ref, W, H, B, bx, by, 0, 0);
+        int mx = 0, my = 0, pts = 1;
+        for (int dy = -p; dy <= p; dy++) {
+            for (int dx = -p; dx <= p; dx++) {
+                if (dx == 0 && dy == 0) continue;
+                uint32_t v = sad_block(cur, ref, W, H, B, bx, by, dx, dy);
+                pts++;
+                if (v < best) { best = v; mx = dx; my = dy; }
+            }
+        }
+        if (mv_out) { mv_out[2 * i] = (int16_t)mx; mv_out[2 * i + 1] = (int16_t)my; }
+        if (sad_out) sad_out[i] = best;
+        if (points_out) points_out[i] = (uint16_t)pts;  /* (2p+1)^2 under C9 (225) */
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Motion-compensated PSNR (P:342 aspect 4; reading C18).                                 */
+/* ------------------------------------------------------------------------------------ */
+int oracle_mc_psnr(const uint8_t* cur, const uint8_t* ref, int W, int H, int B,
+                   const int16_t* mv, double* psnr_out, uint64_t* sse_out) {
+    if (check_frame(W, H, B) || !cur || !ref || !mv) return -1;
+    int nbx = W / B;
+    uint64_t sse = 0;
+    for (int y = 0; y < H; y++) {
+        for (int x = 0; x < W; x++) {
+            int i = (y / B) * nbx + (x / B);
+            int pred = R(ref, W, H, x + mv[2 * i], y + mv[2 * i + 1]);
+            int d = (int)cur[(long)y * W + x] - pred;
+            sse += (uint64_t)(d * d);
+        }
+    }
+    if (sse_out) *sse_out = sse;
+    if (psnr_out) {
+        if (sse == 0) *psnr_out = INFINITY;
+        else *psnr_out = 10.0 * log10((255.0 * 255.0) * ((double)W * H) / (double)sse);
+    }
+    return 0;
+}

@@ -1,0 +1,383 @@
+"""Pins of the CPU oracle to the paper and to mathematics (-m "not gpu").
+
+Each test names the PAPER.md passage (P:n) or the closed form / invariant / brute force that
+fixes the expected value.  None of the expected values comes from the CUDA path.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_0806_0689_b200 import synth
+from _golden import golden_matrix
+
+
+def euclid(t):
+    tx, ty = t
+    return lambda dx, dy: math.hypot(dx - tx, dy - ty)
+
+
+# ---------------------------------------------------------------------------------------
+# Table VII: 64 published integers, ideal Euclidean surface, p = 7.
+# ---------------------------------------------------------------------------------------
+
+def test_table7_dcds_ideal_cost():
+    table7 = golden_matrix("table7_dcds.txt", int)
+    nsp, mx, my = oracle.ideal_nsp_map(7)
+    np.testing.assert_array_equal(nsp[7:, 7:], table7)
+
+
+@pytest.mark.parametrize("p", [7, 15, 16, 32])
+def test_ideal_surface_true_mv_found(p):
+    """DCDS converges to the unique minimum of every unimodal surface (P:301 assumption):
+    the found MV equals the true MV for every (2p+1)^2 placement."""
+    nsp, mx, my = oracle.ideal_nsp_map(p)
+    ty, tx = np.mgrid[-p:p + 1, -p:p + 1]
+    np.testing.assert_array_equal(mx, tx)
+    np.testing.assert_array_equal(my, ty)
+    assert nsp.min() == 7
+
+
+def test_table7_via_single_searches():
+    """Same table through oracle_dcds_cost one placement at a time (independent of the map
+    helper's loop)."""
+    table7 = golden_matrix("table7_dcds.txt", int)
+    for ty in range(8):
+        for tx in range(8):
+            mv, c, pts, _ = oracle.dcds_cost(euclid((tx, ty)), 7)
+            assert mv == (tx, ty) and c == 0.0
+            assert pts == table7[ty, tx], (tx, ty)
+
+
+# ---------------------------------------------------------------------------------------
+# P:297 (III.C.1) and Eq. 8, Fig. 6 example.
+# ---------------------------------------------------------------------------------------
+
+def test_halfway_stop_seven_points():
+    """'If the motion vector is zero, the DCDS algorithm will stop at the first step,
+    and only seven points need to be checked.'"""
+    mv, _, pts, trace = oracle.dcds_cost(euclid((0, 0)), 7)
+    assert mv == (0, 0) and pts == 7
+    assert {r[0] for r in trace} == {0}          # only Step 1 ran
+    assert sorted((r[1], r[2]) for r in trace) == sorted(
+        [(0, 0), (-1, 0), (1, 0), (-2, 0), (2, 0), (0, -1), (0, 1)])   # HCSP, 7 points
+
+
+@pytest.mark.parametrize("t,n", [((1, 0), 10), ((-1, 0), 10), ((0, 1), 11), ((0, -1), 11)])
+def test_p297_ten_or_eleven(t, n):
+    """'(+-1,0) or (0,+-1), the search process will only check 10 or 11 points'."""
+    mv, _, pts, _ = oracle.dcds_cost(euclid(t), 7)
+    assert mv == t and pts == n
+
+
+def _passes(trace):
+    return max(r[0] for r in trace)
+
+
+@pytest.mark.parametrize("t,npts,n_inter,branch", [
+    ((2, 0), 11, 1, 1),   # 7 + 3*1 + 1
+    ((4, 0), 15, 2, 2),   # 7 + 3*2 + 2  (CSP maintained)
+    ((1, 3), 17, 3, 1),   # Fig. 6 example: 7 + 3*3 + 1
+])
+def test_eq8_branches(t, npts, n_inter, branch):
+    """Eq. 8: N = 7 + 3n + 1 (CSP changes in the last step) or 7 + 3n + 2 (CSP
+    maintained), n = number of intermediate steps (Step 2 or Step 3)."""
+    mv, _, pts, trace = oracle.dcds_cost(euclid(t), 7)
+    assert mv == t
+    assert pts == npts == 7 + 3 * n_inter + branch
+    last = _passes(trace)
+    assert last == n_inter + 1                      # passes 1..n intermediate, n+1 = Step 4
+    per_pass = [sum(1 for r in trace if r[0] == k) for k in range(last + 1)]
+    assert per_pass[0] == 7                          # HCSP
+    assert all(v == 3 for v in per_pass[1:-1])       # 'always three' new points
+    assert per_pass[-1] == branch                    # middle points actually scored
+
+
+def test_fig6_trace_reading():
+    """Hand trace of the Fig. 6 example MV (1,3) under Steps 1-4 and the
+    switching strategies: S1 -> (0,1); Step 2 VDSP@(0,1) -> (0,3) (distant,
+    keep VDSP); Step 3 VDSP@(0,3) -> (1,3) (near, switch); HDSP@(1,3) -> centre; Step 4."""
+    _, _, _, trace = oracle.dcds_cost(euclid((1, 3)), 7)
+    by_pass = {}
+    for k, dx, dy, kind in trace:
+        by_pass.setdefault(k, []).append((dx, dy, kind))
+    assert by_pass[1] == [(-1, 1, 2), (1, 1, 2), (0, 3, 2)]          # VDSP at (0,1); (0,-1),(0,1) known
+    assert by_pass[2] == [(-1, 3, 2), (1, 3, 2), (0, 5, 2)]          # VDSP at (0,3)
+    assert by_pass[3] == [(3, 3, 1), (1, 2, 1), (1, 4, 1)]           # HDSP at (1,3)
+    assert by_pass[4] == [(2, 3, 3)]                                   # middle (0,3) already seen
+
+
+def test_window_clipping_not_counted():
+    """Pattern points outside +-p are skipped and not counted (reading C8; Table VII edge
+    entry (7,0) -> 17 requires it)."""
+    mv, _, pts, trace = oracle.dcds_cost(euclid((7, 0)), 7)
+    assert mv == (7, 0) and pts == 17
+    assert all(abs(r[1]) <= 7 and abs(r[2]) <= 7 for r in trace)
+
+
+def test_p1_window():
+    """p = 1: HCSP loses (+-2,0) (infeasible); a zero MV costs 5 points."""
+    _, _, pts, _ = oracle.dcds_cost(euclid((0, 0)), 1)
+    assert pts == 5
+    nsp, mx, my = oracle.ideal_nsp_map(1)
+    ty, tx = np.mgrid[-1:2, -1:2]
+    assert (mx == tx).all() and (my == ty).all()
+
+
+def test_table8_distribution2():
+    """Table VIII: ANSP of DCDS under distribution 2 (Table II weights)
+    prints 9.7.  Table II is quarter-folded, so each cell weights the NSP of (|dx|,|dy|)."""
+    t2 = golden_matrix("table2_mvp.txt", float)
+    nsp, _, _ = oracle.ideal_nsp_map(7)
+    q = nsp[7:, 7:]
+    # the map is symmetric in sign, so the quarter value stands for every sign combination
+    assert (nsp[7:, 7:] == nsp[7:, 7::-1]).all() and (nsp[7:, 7:] == nsp[7::-1, 7:]).all()
+    ansp = float((t2 * q).sum() / t2.sum())
+    assert round(ansp, 1) == 9.7
+
+
+# ---------------------------------------------------------------------------------------
+# Pixel path: the SAD surface of a constructed frame is B*|q-t|^2 + K, so Table VII must
+# come out of oracle_dcds (pixels, clamp, SAD) too.
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("B", [16, 8])
+def test_pixel_ideal_mosaic_reproduces_table7(B):
+    cur, ref, tile, off, blocks = synth.ideal_mosaic(B, 7)
+    mv, sad, pts = oracle.dcds(cur, ref, B, 7)
+    table7 = golden_matrix("table7_dcds.txt", int)
+    got = pts[blocks]
+    np.testing.assert_array_equal(got[7:, 7:], table7)
+    nsp, _, _ = oracle.ideal_nsp_map(7)
+    np.testing.assert_array_equal(got, nsp)
+    ty, tx = np.mgrid[-7:8, -7:8]
+    np.testing.assert_array_equal(mv[blocks][..., 0], tx)
+    np.testing.assert_array_equal(mv[blocks][..., 1], ty)
+
+
+@pytest.mark.parametrize("B", [16, 8])
+def test_pixel_ideal_sad_surface(B):
+    """The mosaic's SAD at q equals B*|q-t|^2 + K (checked by brute SAD of the oracle)."""
+    cur, ref, tile, off, blocks = synth.ideal_mosaic(B, 7)
+    nbx = cur.shape[1] // B
+    for (ty, tx) in [(7, 7), (0, 14), (10, 3)]:
+        i = blocks[ty, tx]
+        bx, by = (i % nbx) * B, (i // nbx) * B
+        t = (tx - 7, ty - 7)
+        base = oracle.sad(cur, ref, B, bx, by, *t)
+        for dy in range(-7, 8):
+            for dx in range(-7, 8):
+                s = oracle.sad(cur, ref, B, bx, by, dx, dy)
+                assert s == base + B * ((dx - t[0]) ** 2 + (dy - t[1]) ** 2)
+
+
+# ---------------------------------------------------------------------------------------
+# SAD / SSE / PSNR against hand examples, closed forms and an independent brute force.
+# ---------------------------------------------------------------------------------------
+
+def test_sad_hand_examples():
+    a = np.array([[1, 2], [3, 4]], np.uint8)
+    b = np.array([[0, 2], [3, 6]], np.uint8)
+    assert oracle.sad(a, b, 2, 0, 0, 0, 0) == 3                  # 1+0+0+2
+    assert oracle.sse_block(a, b, 2, 0, 0, 0, 0) == 5             # 1+0+0+4 (MSE 1.25)
+    f5 = np.full((16, 16), 5, np.uint8)
+    f7 = np.full((16, 16), 7, np.uint8)
+    assert oracle.sad(f5, f7, 16, 0, 0, 0, 0) == 512             # 256 * |5-7|
+    assert oracle.sse_block(f5, f7, 16, 0, 0, 0, 0) == 1024       # MSE 4.0
+
+
+def _brute_sad(cur, ref, B, bx, by, dx, dy):
+    H, W = ref.shape
+    pad = 80
+    rp = np.pad(ref.astype(np.int64), pad, mode="edge")     # edge replication (reading C9)
+    blk = cur[by:by + B, bx:bx + B].astype(np.int64)
+    win = rp[pad + by + dy: pad + by + dy + B, pad + bx + dx: pad + bx + dx + B]
+    return int(np.abs(blk - win).sum())
+
+
+def test_sad_matches_brute_force_with_clamp():
+    cur, ref = synth.random_pair(48, 32, seed=3)
+    rng = np.random.default_rng(0)
+    for _ in range(300):
+        B = int(rng.choice([8, 16]))
+        bx = int(rng.integers(0, 48 // B)) * B
+        by = int(rng.integers(0, 32 // B)) * B
+        dx, dy = (int(v) for v in rng.integers(-40, 41, 2))
+        assert oracle.sad(cur, ref, B, bx, by, dx, dy) == _brute_sad(cur, ref, B, bx, by, dx, dy)
+
+
+def test_psnr_closed_forms():
+    f5 = np.full((32, 48), 5, np.uint8)
+    f7 = np.full((32, 48), 7, np.uint8)
+    mv = np.zeros((6, 2), np.int16)
+    ps, sse = oracle.mc_psnr(f5, f7, 16, mv)
+    assert sse == 4 * 32 * 48
+    assert ps == pytest.approx(10 * math.log10(65025 / 4), abs=1e-12)
+    assert round(ps, 2) == 42.11
+    ps1, _ = oracle.mc_psnr(f7, f7 - 1, 16, mv)
+    assert ps1 == pytest.approx(10 * math.log10(65025.0), abs=1e-12)
+    assert round(ps1, 2) == 48.13
+    psi, ssei = oracle.mc_psnr(f7, f7, 16, mv)
+    assert ssei == 0 and math.isinf(psi)
+
+
+def test_mc_psnr_brute_force():
+    cur, ref = synth.random_pair(64, 48, seed=5)
+    B = 16
+    rng = np.random.default_rng(1)
+    mv = rng.integers(-20, 21, ((64 // B) * (48 // B), 2)).astype(np.int16)
+    ps, sse = oracle.mc_psnr(cur, ref, B, mv)
+    tot = 0
+    for i, (dx, dy) in enumerate(mv):
+        bx, by = (i % 4) * B, (i // 4) * B
+        pad = 40
+        rp = np.pad(ref.astype(np.int64), pad, mode="edge")
+        win = rp[pad + by + dy: pad + by + dy + B, pad + bx + dx: pad + bx + dx + B]
+        tot += int(((cur[by:by + B, bx:bx + B].astype(np.int64) - win) ** 2).sum())
+    assert sse == tot
+    assert ps == pytest.approx(10 * math.log10(255.0 ** 2 * 64 * 48 / tot), abs=1e-12)
+
+
+# ---------------------------------------------------------------------------------------
+# Full search: definition (argmin over the window) checked by an independent brute force.
+# ---------------------------------------------------------------------------------------
+
+def _brute_fs(cur, ref, B, p):
+    H, W = cur.shape
+    nbx, nby = W // B, H // B
+    out_mv, out_sad = [], []
+    for i in range(nbx * nby):
+        bx, by = (i % nbx) * B, (i // nbx) * B
+        S = np.array([[_brute_sad(cur, ref, B, bx, by, dx, dy) for dx in range(-p, p + 1)]
+                      for dy in range(-p, p + 1)])
+        m = S.min()
+        if S[p, p] == m:
+            mv = (0, 0)                                   # centre first (reading C13)
+        else:
+            k = int(np.flatnonzero(S.ravel() == m)[0])      # then raster order
+            mv = (k % (2 * p + 1) - p, k // (2 * p + 1) - p)
+        out_mv.append(mv)
+        out_sad.append(m)
+    return np.array(out_mv), np.array(out_sad)
+
+
+@pytest.mark.parametrize("B,p,kind", [(16, 2, "random"), (8, 3, "random"), (8, 2, "binary"),
+                                      (16, 1, "flat"), (8, 4, "texture")])
+def test_fullsearch_brute_force(B, p, kind):
+    W, H = 48, 32
+    if kind == "random":
+        cur, ref = synth.random_pair(W, H, seed=11)
+    elif kind == "binary":
+        cur, ref = synth.binary_pair(W, H, seed=12)
+    elif kind == "flat":
+        cur, ref = synth.flat_pair(W, H)
+    else:
+        tex = synth.texture(W, H, (2.0,), seed=13).numpy()
+        cur, ref = synth.translated_pair(tex, 1, -2)
+    mv, sad, pts = oracle.fullsearch(cur, ref, B, p)
+    bmv, bsad = _brute_fs(cur, ref, B, p)
+    np.testing.assert_array_equal(sad, bsad)
+    np.testing.assert_array_equal(mv, bmv)
+    assert (pts == (2 * p + 1) ** 2).all()              # every candidate scorable (C9)
+
+
+def test_fullsearch_translation_closed_form():
+    """Zero-noise translation: interior blocks recover the exact shift with SAD 0."""
+    tex = synth.texture(128, 96, (2.0,), seed=21).numpy()
+    for (dx, dy) in [(3, 0), (-2, 1), (0, -4), (5, 5)]:
+        cur, ref = synth.translated_pair(tex, dx, dy)
+        mv, sad, pts = oracle.fullsearch(cur, ref, 16, 7)
+        nbx = 128 // 16
+        for i in range(len(mv)):
+            bx, by = (i % nbx) * 16, (i // nbx) * 16
+            if 16 <= bx <= 128 - 32 and 16 <= by <= 96 - 32:
+                assert tuple(mv[i]) == (dx, dy) and sad[i] == 0
+
+
+def test_fs_nsp_225_everywhere():
+    """FS NSP is 225 for +-7, including border blocks (reading C9)."""
+    cfg = synth.CONFIGS["c0"]
+    fr = synth.make_sequence(cfg).numpy()
+    _, _, pts = oracle.fullsearch(fr[0, 0], fr[0, 1], 16, 7)
+    assert (pts == 225).all()
+
+
+# ---------------------------------------------------------------------------------------
+# DCDS vs FS invariants; identical frames; DCDS^S.
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind", ["c0", "random", "binary", "flat"])
+def test_dcds_never_beats_fs(kind):
+    """FS is the exhaustive minimum: SAD_FS <= SAD_DCDS on every block."""
+    if kind == "c0":
+        fr = synth.make_sequence(synth.CONFIGS["c0"]).numpy()
+        cur, ref = fr[0, 0], fr[0, 1]
+    elif kind == "random":
+        cur, ref = synth.random_pair(176, 144, seed=31)
+    elif kind == "binary":
+        cur, ref = synth.binary_pair(176, 144, seed=32)
+    else:
+        cur, ref = synth.flat_pair(176, 144)
+    for B in (16, 8):
+        mv, sad, pts = oracle.dcds(cur, ref, B, 7)
+        fmv, fsad, _ = oracle.fullsearch(cur, ref, B, 7)
+        assert (sad >= fsad).all()
+        assert (pts >= 5).all() and (pts <= 225).all()
+        # the returned SAD is the SAD at the returned MV
+        nbx = 176 // B
+        for i in range(0, len(mv), 7):
+            assert sad[i] == oracle.sad(cur, ref, B, (i % nbx) * B, (i // nbx) * B, *mv[i])
+
+
+def test_identical_frames():
+    """Static content: every block stops in Step 1 with 7 points (reading C9)."""
+    fr = synth.make_sequence(synth.CONFIGS["c0"]).numpy()
+    ref = fr[0, 1]
+    mv, sad, pts = oracle.dcds(ref, ref, 16, 7)
+    assert (mv == 0).all() and (sad == 0).all() and (pts == 7).all()
+    fmv, fsad, fpts = oracle.fullsearch(ref, ref, 16, 7)
+    assert (fmv == 0).all() and (fsad == 0).all() and (fpts == 225).all()
+
+
+@pytest.mark.parametrize("octaves,min_rate", [((2.0,), 0.99), ((1.0, 4.0, 16.0), 0.995)])
+def test_dcds_equals_fs_on_small_translations(octaves, min_rate):
+    """North star: DCDS = FS on zero-noise small translations.  Statistical on a sigma=2
+    texture (SURVEY finding 7: a few blocks stick in a local minimum) and on the seeded
+    3-octave texture too (1 of 2000 interior blocks sticks at this seed).  Interior blocks,
+    |d| <= 2.  FS itself must be exact (closed form: SAD 0 at the shift)."""
+    tex = synth.texture(192, 160, octaves, seed=41).numpy()
+    hit = tot = 0
+    for dy in range(-2, 3):
+        for dx in range(-2, 3):
+            cur, ref = synth.translated_pair(tex, dx, dy)
+            mv, sad, _ = oracle.dcds(cur, ref, 16, 7)
+            fmv, fsad, _ = oracle.fullsearch(cur, ref, 16, 7)
+            nbx = 192 // 16
+            for i in range(len(mv)):
+                bx, by = (i % nbx) * 16, (i // nbx) * 16
+                if 16 <= bx <= 192 - 32 and 16 <= by <= 160 - 32:
+                    tot += 1
+                    assert tuple(fmv[i]) == (dx, dy) and fsad[i] == 0
+                    hit += int(tuple(mv[i]) == (dx, dy))
+    assert hit / tot >= min_rate
+
+
+def test_dcds_simplified_variant():
+    """DCDS^S: Step 4 checks at most one middle point, so NSP(S) <= NSP(DCDS) per
+    block; zero MV -> 7, (1,0) -> 10."""
+    n0, _, _ = oracle.ideal_nsp_map(7, 0)
+    n1, _, _ = oracle.ideal_nsp_map(7, 1)
+    assert (n1 <= n0).all() and n1[7, 7] == 7 and n1[7, 8] == 10
+    fr = synth.make_sequence(synth.CONFIGS["c0"]).numpy()
+    _, s0, p0 = oracle.dcds(fr[0, 0], fr[0, 1], 16, 7, 0)
+    _, s1, p1 = oracle.dcds(fr[0, 0], fr[0, 1], 16, 7, 1)
+    assert (p1 <= p0).all()
+
+
+def test_invalid_arguments():
+    cur, ref = synth.flat_pair(48, 32)
+    with pytest.raises(ValueError):
+        oracle.dcds(cur[:, :40], ref[:, :40], 16, 7)
+    with pytest.raises(ValueError):
+        oracle.dcds(cur, ref, 16, 0)
