@@ -1,0 +1,394 @@
+"""bench.py -- DCDS throughput on B200 (BASELINE.json metric: DCDS macroblocks/s and 1080p
+frames/s per GPU and across GPUs, with the fraction of roofline).
+
+Workload (N=1 default): config c3 -- 1920x1088 8-bit luma, 8x8 blocks, +-16 window, 239
+independent frame pairs per GPU (the metric names 1080p frames/s).  A step is one pass of the
+hot path over the batch: DCDS search of every block of every pair (Steps 1-4) with the fused
+motion-compensated SSE and per-pair statistics (sum NSP, sum SAD, SSE), one launch through
+the C ABI (me_dcds_batch); with N > 1 the per-pair MV fields and statistics are then gathered
+with NCCL (the only collective; BASELINE.json north_star).  Full search (the quality
+reference) is timed separately in the same run and reported under "fullsearch".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_0806_0689_b200 import synth  # noqa: E402
+
+METRIC = "DCDS macroblocks/sec"
+UNIT = "blocks/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    ap.add_argument("--no-fs", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region (nvidia-smi sampler)
+# ------------------------------------------------------------------------------------------
+REASON_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[3], 16)
+            except ValueError:
+                continue
+            for b, n in REASON_BITS.items():
+                if bits & b and n != "gpu_idle":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_int_peak():
+    """Measured VABSDIFF4 lane-op rate (profiles/int_peaks.json, tools/int_peaks.cu)."""
+    p = os.path.join(ROOT, "profiles", "int_peaks.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["vabsdiff4_add"]["lane_ops_per_sm_per_clk"], d.get("sms", 148)
+    return None, 148
+
+
+# ------------------------------------------------------------------------------------------
+# the oracle, timed on host cores (cpu_baseline leg and --impl reference)
+# ------------------------------------------------------------------------------------------
+def oracle_rate(frames_host: np.ndarray, cfg, budget_s: float):
+    import oracle  # test infrastructure; only this leg of bench.py may use it
+    oracle.build()
+    n = 0
+    blocks = 0
+    t0 = time.perf_counter()
+    while n < frames_host.shape[0]:
+        oracle.dcds(frames_host[n, 0], frames_host[n, 1], cfg.B, cfg.p)
+        n += 1
+        blocks += cfg.nb
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return blocks / dt, n, dt
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, single-threaded on the host, one bounded
+    sample (one pair) per step, on the same config/metric/unit as the b200 arm."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    dev = "cuda:0" if torch.cuda.is_available() else "cpu"
+    k = args.steps + args.warmup
+    npairs = min(cfg.npairs, max(1, k))
+    fr = synth.make_sequence(cfg, device=dev, pairs=range(1, npairs + 1)).cpu().numpy()
+    import oracle
+    oracle.build()
+    times = []
+    for s in range(k):
+        t0 = time.perf_counter()
+        oracle.dcds(fr[s % npairs, 0], fr[s % npairs, 1], cfg.B, cfg.p)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = cfg.nb * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded; SURVEY 8(d) generator)",
+        "config": {"workload": f"{cfg.name}: {cfg.W}x{cfg.H}, {cfg.B}x{cfg.B} blocks, +-{cfg.p}",
+                   "sample_per_step": "1 frame pair"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"1 pair per step, {len(times)} steps; {cpu_model()}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# the B200 arm
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_0806_0689_b200 as me
+    me.me_init(local)
+    stream = torch.cuda.current_stream()
+    me.me_set_stream(stream)
+
+    cfg = synth.CONFIGS[args.config]
+    # weak scaling: every rank searches its own cfg.npairs pairs (pair indices offset by rank)
+    n = cfg.npairs
+    pairs = range(1 + rank * n, 1 + (rank + 1) * n)
+    frames = synth.make_sequence(cfg, device=dev, pairs=pairs)
+    mv, sad, pts, st = me.alloc_outputs(n, cfg.nb, dev)
+    in_bytes = frames.numel()
+    torch.cuda.synchronize()
+
+    if ws > 1:
+        import torch.distributed as dist
+        # one packed record per block: mv (4 B) + sad (4 B) + points (2 B), plus per-pair stats
+        g_mv = torch.empty(ws * n * cfg.nb * 2, dtype=torch.int16, device=dev)
+        g_sad = torch.empty(ws * n * cfg.nb, dtype=torch.int32, device=dev)
+        g_pts = torch.empty(ws * n * cfg.nb, dtype=torch.int16, device=dev)
+        g_st = torch.empty(ws * n * 3, dtype=torch.int64, device=dev)
+
+    def step():
+        me.me_dcds_batch(frames, cfg.B, cfg.p, mv, sad, pts, st)
+        if ws > 1:
+            dist.all_gather_into_tensor(g_mv, mv.view(-1))
+            dist.all_gather_into_tensor(g_sad, sad.view(-1))
+            dist.all_gather_into_tensor(g_pts, pts.view(-1))
+            dist.all_gather_into_tensor(g_st, st.view(-1))
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches0 = me.me_launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            me.me_dcds_batch(frames, cfg.B, cfg.p, mv, sad, pts, st)
+            ev[k][1].record(stream)
+            if ws > 1:
+                dist.all_gather_into_tensor(g_mv, mv.view(-1))
+                dist.all_gather_into_tensor(g_sad, sad.view(-1))
+                dist.all_gather_into_tensor(g_pts, pts.view(-1))
+                dist.all_gather_into_tensor(g_st, st.view(-1))
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = me.me_launch_count() - launches0
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / args.steps
+    stats = st.cpu().numpy().astype(np.float64)
+    sum_pts = float(stats[:, 0].sum())
+    blocks_per_step_rank = n * cfg.nb
+    value = ws * blocks_per_step_rank / (ms_per_step * 1e-3)
+
+    # roofline of the dominant kernel (dcds_kernel), algorithmic bytes / ops per launch
+    hbm_peak, hbm_src = load_peaks()
+    kern_avg_s = statistics.mean(kern_ms) * 1e-3
+    bytes_per_pair = 2 * cfg.W * cfg.H + 10 * cfg.nb + 24
+    alg_bytes = n * bytes_per_pair
+    achieved_gbs = alg_bytes / kern_avg_s / 1e9
+    lane_ops = sum_pts * cfg.B * cfg.B / 4.0            # VABSDIFF4 lane-ops the method needs
+    r_clk, sms = load_int_peak()
+    clocks = clk.summary()
+    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved_gbs / hbm_peak, "traffic": None, "peak_source": hbm_src,
+                "alg_bytes_per_launch": alg_bytes}
+    if r_clk is not None:
+        clk_mhz = clocks["sm_mhz"] or 1965.0
+        int_peak = r_clk * sms * clk_mhz * 1e6          # lane-ops/s at the clock seen
+        t_hbm = alg_bytes / (hbm_peak * 1e9)
+        t_int = lane_ops / int_peak
+        roofline["int_peak_lane_ops_per_s"] = int_peak
+        roofline["int_achieved_lane_ops_per_s"] = lane_ops / kern_avg_s
+        roofline["t_roof_ms"] = {"hbm": t_hbm * 1e3, "alu": t_int * 1e3}
+        if t_int > t_hbm:
+            roofline.update({"bound": "alu", "achieved": lane_ops / kern_avg_s / 1e12,
+                             "peak": int_peak / 1e12, "unit": "Tlane-op/s",
+                             "frac": (lane_ops / kern_avg_s) / int_peak,
+                             "peak_source": "measured VABSDIFF4 rate (profiles/int_peaks.json) x SMs x median SM clock"})
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        d = json.load(open(tp)).get(cfg.name)
+        if d:
+            roofline["traffic"] = d.get("dram_bytes_per_launch")
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded; SURVEY 8(d) generator; paper's sequences unavailable)",
+        "config": {
+            "workload": f"{cfg.name}: {cfg.W}x{cfg.H} luma, {cfg.B}x{cfg.B} blocks, +-{cfg.p} window, "
+                        f"{n} frame pairs per GPU",
+            "pairs_per_gpu": n, "blocks_per_pair": cfg.nb, "W": cfg.W, "H": cfg.H,
+            "block": cfg.B, "p": cfg.p,
+            "frames_per_sec": ws * n / (ms_per_step * 1e-3),
+            "mean_nsp": sum_pts / (n * cfg.nb),
+            "l2": f"inputs {in_bytes / 2**20:.0f} MiB per GPU > 126 MB L2 (no flush needed)",
+            "parallelism": f"dp{ws} (frame pairs sharded; NCCL all_gather of MV fields + stats)"
+                           if ws > 1 else "single GPU",
+        },
+        "gpu_launches": int(launches),
+        "kernel_ms_mean": statistics.mean(kern_ms),
+        "roofline": roofline,
+        "clocks": clocks,
+    }
+
+    if rank == 0 and not args.no_fs:
+        # FS (quality reference), same pairs, small sample: timed beside the path
+        nfs = min(n, 4)
+        fsub = frames[:nfs]
+        fo = me.alloc_outputs(nfs, cfg.nb, dev)
+        me.me_fullsearch_batch(fsub, cfg.B, cfg.p, *fo)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        a.record(stream)
+        for _ in range(reps):
+            me.me_fullsearch_batch(fsub, cfg.B, cfg.p, *fo)
+        b.record(stream)
+        torch.cuda.synchronize()
+        fs_s = a.elapsed_time(b) * 1e-3 / reps
+        fs_ops = nfs * cfg.nb * (2 * cfg.p + 1) ** 2 * cfg.B * cfg.B / 4.0
+        fsline = {"value": nfs * cfg.nb / fs_s, "unit": UNIT, "pairs": nfs, "ms": fs_s * 1e3,
+                  "lane_ops_per_s": fs_ops / fs_s}
+        if r_clk is not None:
+            fsline["alu_frac"] = (fs_ops / fs_s) / roofline["int_peak_lane_ops_per_s"]
+        line["fullsearch"] = fsline
+
+    if rank == 0 and not args.no_e2e:
+        # end to end through the C ABI on HOST buffers: H2D of the frames (pinned), search,
+        # D2H of the MV field + stats, every step
+        hfr = frames.cpu().pin_memory()
+        hout = [t.pin_memory() for t in me.alloc_outputs(n, cfg.nb, "cpu")]
+        me.me_dcds_batch_host(hfr, cfg.B, cfg.p, *hout)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            me.me_dcds_batch_host(hfr, cfg.B, cfg.p, *hout)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_s = a.elapsed_time(b) * 1e-3 / args.e2e_steps
+        assert np.array_equal(hout[0].numpy(), mv.cpu().numpy())
+        line["e2e"] = {"value": n * cfg.nb / e2e_s, "unit": UNIT,
+                       "h2d_bytes_per_step": int(in_bytes),
+                       "d2h_bytes_per_step": int(n * (cfg.nb * 10 + 24)),
+                       "ms_per_step": e2e_s * 1e3, "steps": args.e2e_steps}
+
+    if rank == 0 and not args.no_cpu and ws == 1:
+        host = frames[: min(n, 64)].cpu().numpy()
+        rate, npairs_done, dt = oracle_rate(host, cfg, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"{npairs_done} pairs of {cfg.name} ({npairs_done * cfg.nb} blocks) "
+                                          f"in {dt:.1f} s, single thread, gcc -O2; {cpu_model()}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

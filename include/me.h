@@ -1,0 +1,130 @@
+/*
+ * me.h -- C ABI of libme.so, the B200 (sm_100a) DCDS block-motion-estimation hot path.
+ *
+ * Paper: Jia & Zhang, "Directional Cross Diamond Search Algorithm for Fast Block Motion
+ * Estimation" (arxiv 0806.0689); P:n = PAPER.md line n.  DESIGN.md states the readings.
+ *
+ * Problem statement: "The frame is partitioned into non-overlapping and equal-sized
+ * blocks (8x8) or macroblocks (16x16) ... the motion vector is obtained by finding out the
+ * displacement of the best-matched block in the reference frame ... within the search window
+ * centered around the original position.  Matching process is performed by minimizing a
+ * certain matching criterion."
+ *
+ * Common conventions (every entry point):
+ *   - Frames are 8-bit luma, row-major, pitch = W bytes.  W % block == 0, H % block == 0,
+ *     block in {8, 16}; W % 16 == 0 and every frame/base pointer 16-byte aligned
+ *     (vectorised loads) -- else ME_EALIGN.
+ *   - Blocks are numbered in raster order; nb = (W/block) * (H/block).
+ *   - MV convention: cur block at (bx,by) matches ref at (bx+dx, by+dy).  mv arrays hold
+ *     int16 pairs (dx, dy) per block ([nb][2]).
+ *   - Candidates are limited to |dx|,|dy| <= p with 1 <= p <= 32.  Reference pixels outside
+ *     the frame read the edge-replicated reference ref[clamp(y)][clamp(x)] (reading C9), so
+ *     every window candidate is scorable.
+ *   - SAD = sum over the block of |cur - ref| (integer; the paper's MAD times block^2,
+ *     P:342; reading C12).  Ties keep the incumbent; among new points the first in the fixed
+ *     pattern order wins (readings C6, C7; FS: centre first then raster, C13).
+ *   - Pointers are DEVICE pointers unless marked (host).  The caller owns every buffer and
+ *     keeps inputs alive until the stream completes; the library allocates nothing per call
+ *     (the _host variant keeps grow-only staging buffers, freed by me_shutdown).
+ *   - All launches are asynchronous on the stream set by me_set_stream (default: the legacy
+ *     default stream) unless the entry point says it synchronises.
+ *   - Errors: a negative me_status; arguments are validated before any device work, and no
+ *     partial outputs are promised after an error.  CUDA errors map to ME_ECUDA and
+ *     me_strerror() returns the detail of the last error.  Not thread-safe: one host thread
+ *     drives the library per process.  There is no CPU fallback.
+ */
+#ifndef ME_H
+#define ME_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ME_OK = 0,
+    ME_EINVAL = -1,    /* bad sizes / block / p / npairs / NULL pointer                  */
+    ME_EALIGN = -2,    /* W % 16 != 0 or a pointer / stride not 16-byte aligned           */
+    ME_ENOTINIT = -3,  /* me_init has not succeeded                                       */
+    ME_ECUDA = -4,     /* a CUDA runtime error (see me_strerror)                          */
+    ME_ENOMEM = -5     /* device allocation failed (host-buffer variant only)             */
+} me_status;
+
+/* Select `device`, check it is sm_100 with enough shared memory, set kernel attributes.
+ * Idempotent per device. */
+int me_init(int device);
+
+/* cudaStream_t for every later launch (NULL = legacy default stream). */
+int me_set_stream(void* cuda_stream);
+
+/* DCDS on one frame pair: Step 1 HCSP with the halfway stop,
+ * Step 2 HDSP/VDSP by switching strategy one, Step 3 repeated with switching
+ * strategy two until the BMP is the pattern centre (no iteration cap), Step 4
+ * the two middle points.  Each position is scored at most once per block
+ * (reading C5).
+ * Outputs per block: mv_out [nb][2] int16 (dx,dy); sad_out [nb] SAD at that MV;
+ * points_out [nb] number of distinct candidates scored (NSP, P:342 aspect 3). */
+int me_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int block, int p,
+            int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out);
+
+/* Full search: all (2p+1)^2 window candidates, (0,0) first then raster (dy outer,
+ * dx inner), strict minimum.  points_out = (2p+1)^2 for every block ("225"). */
+int me_fullsearch(const uint8_t* cur, const uint8_t* ref, int W, int H, int block, int p,
+                  int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out);
+
+/* Motion-compensated PSNR of cur predicted from ref by the mv field (P:342 aspect 4):
+ * SSE = sum (cur(x,y) - ref(clamp(x+dx), clamp(y+dy)))^2 (exact, uint64); *psnr_out =
+ * 10*log10(255^2*W*H/SSE) in double (+inf when SSE == 0; reading C18).  psnr_out and
+ * sse_out are HOST pointers (sse_out may be NULL).  Synchronises the stream. */
+int me_mc_psnr(const uint8_t* cur, const uint8_t* ref, int W, int H, int block,
+               const int16_t* mv, double* psnr_out /* host */, uint64_t* sse_out /* host */);
+
+/* Throughput path: npairs independent pairs; pair t's frames are cur0 + t*pair_stride and
+ * ref0 + t*pair_stride (pair_stride % 16 == 0).  Outputs are concatenated per pair:
+ * mv_out [npairs][nb][2], sad_out [npairs][nb], points_out [npairs][nb].
+ * stats_out (device, may be NULL): [npairs][3] uint64 = {sum points, sum SAD, SSE of the
+ * motion-compensated pair at the DCDS MVs (P:342 aspects 1-4)}; overwritten. */
+int me_dcds_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                  int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
+                  uint16_t* points_out, uint64_t* stats_out);
+
+/* DCDS^S (Table X): as me_dcds_batch but Step 4 scores only the middle point on the
+ * side of the cheaper distant point of the final pattern (an infeasible distant point costs
+ * +inf; a tie picks the negative side -- reading C22). */
+int me_dcds_s_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                    int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
+                    uint16_t* points_out, uint64_t* stats_out);
+
+/* Full search over npairs pairs; same layout as me_dcds_batch (stats: {sum points, sum SAD,
+ * SSE at the FS MVs}). */
+int me_fullsearch_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride,
+                        int npairs, int W, int H, int block, int p, int16_t* mv_out,
+                        uint32_t* sad_out, uint16_t* points_out, uint64_t* stats_out);
+
+/* Motion-compensated SSE of npairs pairs (device sse_out [npairs] uint64, overwritten). */
+int me_mc_sse_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                    int W, int H, int block, const int16_t* mv, uint64_t* sse_out);
+
+/* End-to-end variant of me_dcds_batch on HOST buffers: frames (host, [npairs] x
+ * pair_stride bytes as above) are copied to the device in chunks on two streams,
+ * overlapped with the search of the previous chunk, and the outputs (host) copied back.
+ * Synchronises.  Pinned host memory gives full copy bandwidth.  Returns ME_ENOMEM if the
+ * staging buffers cannot be allocated. */
+int me_dcds_batch_host(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride,
+                       int npairs, int W, int H, int block, int p, int16_t* mv_out,
+                       uint32_t* sad_out, uint16_t* points_out, uint64_t* stats_out);
+
+/* Number of kernels this library has launched since me_init (for the bench's
+ * gpu_launches field). */
+int64_t me_launch_count(void);
+
+/* Static description of the last error (never NULL). */
+const char* me_strerror(int status);
+
+/* Free library-owned device memory and forget the device. */
+void me_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

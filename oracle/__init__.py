@@ -56,11 +56,16 @@ def lib() -> ctypes.CDLL:
         L.oracle_sse_block.argtypes = [u8p, u8p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, u64p]
         L.oracle_dcds.argtypes = [u8p, u8p, c_int, c_int, c_int, c_int, c_int, i16p, u32p, u16p]
         L.oracle_fullsearch.argtypes = [u8p, u8p, c_int, c_int, c_int, c_int, i16p, u32p, u16p]
+        L.oracle_dcds_block.argtypes = [u8p, u8p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                        i16p, u32p, u16p]
+        L.oracle_fullsearch_block.argtypes = [u8p, u8p, c_int, c_int, c_int, c_int, c_int, c_int,
+                                              i16p, u32p, u16p]
         L.oracle_mc_psnr.argtypes = [u8p, u8p, c_int, c_int, c_int, i16p, dp, u64p]
         L.oracle_dcds_cost.argtypes = [COST_FN, ctypes.c_void_p, c_int, c_int, ip, ip, dp, ip, ip, c_int, ip]
         L.oracle_ideal_nsp_map.argtypes = [c_int, c_int, ip, ip, ip]
         for f in (L.oracle_sad, L.oracle_sse_block, L.oracle_dcds, L.oracle_fullsearch,
-                  L.oracle_mc_psnr, L.oracle_dcds_cost, L.oracle_ideal_nsp_map):
+                  L.oracle_mc_psnr, L.oracle_dcds_cost, L.oracle_ideal_nsp_map,
+                  L.oracle_dcds_block, L.oracle_fullsearch_block):
             f.restype = c_int
         _lib = L
     return _lib
@@ -122,6 +127,28 @@ def dcds(cur, ref, B, p, variant: int = 0):
 def fullsearch(cur, ref, B, p):
     """Full search: returns (mv, sad, points) like :func:`dcds`."""
     return _search(lib().oracle_fullsearch, cur, ref, B, p)
+
+
+def _block(fn, cur, ref, B, p, bx, by, *extra):
+    cur, ref = _frames(cur, ref)
+    H, W = cur.shape
+    mv = np.zeros(2, np.int16)
+    s = np.zeros(1, np.uint32)
+    n = np.zeros(1, np.uint16)
+    _check(fn(_ptr(cur, ctypes.c_uint8), _ptr(ref, ctypes.c_uint8), W, H, B, p, *extra, bx, by,
+              _ptr(mv, ctypes.c_int16), _ptr(s, ctypes.c_uint32), _ptr(n, ctypes.c_uint16)),
+           fn.__name__)
+    return (int(mv[0]), int(mv[1])), int(s[0]), int(n[0])
+
+
+def dcds_block(cur, ref, B, p, bx, by, variant: int = 0):
+    """DCDS of the single block at (bx, by): ((dx, dy), sad, points)."""
+    return _block(lib().oracle_dcds_block, cur, ref, B, p, bx, by, variant)
+
+
+def fullsearch_block(cur, ref, B, p, bx, by):
+    """Full search of the single block at (bx, by): ((dx, dy), sad, points)."""
+    return _block(lib().oracle_fullsearch_block, cur, ref, B, p, bx, by)
 
 
 def mc_psnr(cur, ref, B, mv):

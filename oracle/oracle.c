@@ -231,24 +231,34 @@ static double pix_cost(int dx, int dy, void* ctx) {
     return (double)sad_block(c->cur, c->ref, c->W, c->H, c->B, c->bx, c->by, dx, dy);
 }
 
-int oracle_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
-                int variant, int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out) {
+int oracle_dcds_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
+                      int variant, int bx, int by, int16_t* mv_out, uint32_t* sad_out,
+                      uint16_t* points_out) {
     if (check_frame(W, H, B) || p < 1 || !cur || !ref) return -1;
     if (variant != 0 && variant != 1) return -1;
+    if (bx < 0 || by < 0 || bx + B > W || by + B > H) return -1;
     search_t s;
     if (search_init(&s, p)) return -1;
-    pix_ctx c = {cur, ref, W, H, B, 0, 0};
+    pix_ctx c = {cur, ref, W, H, B, bx, by};
     s.cost = pix_cost; s.ctx = &c;
-    int nbx = W / B, nby = H / B;
-    for (int i = 0; i < nbx * nby; i++) {  /* raster order */
-        c.bx = (i % nbx) * B; c.by = (i / nbx) * B;
-        int mx, my; double best;
-        dcds_search(&s, variant, &mx, &my, &best);
-        if (mv_out) { mv_out[2 * i] = (int16_t)mx; mv_out[2 * i + 1] = (int16_t)my; }
-        if (sad_out) sad_out[i] = (uint32_t)best;
-        if (points_out) points_out[i] = (uint16_t)s.points;
-    }
+    int mx, my; double best;
+    dcds_search(&s, variant, &mx, &my, &best);
+    if (mv_out) { mv_out[0] = (int16_t)mx; mv_out[1] = (int16_t)my; }
+    if (sad_out) sad_out[0] = (uint32_t)best;
+    if (points_out) points_out[0] = (uint16_t)s.points;
     search_free(&s);
+    return 0;
+}
+
+int oracle_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
+                int variant, int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out) {
+    if (check_frame(W, H, B) || p < 1 || !cur || !ref || !mv_out || !sad_out || !points_out)
+        return -1;
+    int nbx = W / B, nby = H / B;
+    for (int i = 0; i < nbx * nby; i++)  /* raster order */
+        if (oracle_dcds_block(cur, ref, W, H, B, p, variant, (i % nbx) * B, (i / nbx) * B,
+                              mv_out + 2 * i, sad_out + i, points_out + i))
+            return -1;
     return 0;
 }
 
@@ -300,27 +310,37 @@ int oracle_ideal_nsp_map(int p, int variant, int* nsp_out, int* mvx_out, int* mv
 /* ------------------------------------------------------------------------------------ */
 /* Full search: every candidate of the window; the brute-force quality reference. */
 /* ------------------------------------------------------------------------------------ */
+int oracle_fullsearch_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
+                            int bx, int by, int16_t* mv_out, uint32_t* sad_out,
+                            uint16_t* points_out) {
+    if (check_frame(W, H, B) || p < 1 || !cur || !ref) return -1;
+    if (bx < 0 || by < 0 || bx + B > W || by + B > H) return -1;
+    /* (0,0) first (reading C13), then raster order; strict minimum. */
+    uint32_t best = sad_block(cur, ref, W, H, B, bx, by, 0, 0);
+    int mx = 0, my = 0, pts = 1;
+    for (int dy = -p; dy <= p; dy++) {
+        for (int dx = -p; dx <= p; dx++) {
+            if (dx == 0 && dy == 0) continue;
+            uint32_t v = sad_block(cur, ref, W, H, B, bx, by, dx, dy);
+            pts++;
+            if (v < best) { best = v; mx = dx; my = dy; }
+        }
+    }
+    if (mv_out) { mv_out[0] = (int16_t)mx; mv_out[1] = (int16_t)my; }
+    if (sad_out) sad_out[0] = best;
+    if (points_out) points_out[0] = (uint16_t)pts;  /* (2p+1)^2 under C9 (225) */
+    return 0;
+}
+
 int oracle_fullsearch(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
                       int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out) {
-    if (check_frame(W, H, B) || p < 1 || !cur || !ref) return -1;
+    if (check_frame(W, H, B) || p < 1 || !cur || !ref || !mv_out || !sad_out || !points_out)
+        return -1;
     int nbx = W / B, nby = H / B;
-    for (int i = 0; i < nbx * nby; i++) {
-        int bx = (i % nbx) * B, by = (i / nbx) * B;
-        /* (0,0) first (reading C13), then raster order; strict minimum. */
-        uint32_t best = sad_block(cur, ref, W, H, B, bx, by, 0, 0);
-        int mx = 0, my = 0, pts = 1;
-        for (int dy = -p; dy <= p; dy++) {
-            for (int dx = -p; dx <= p; dx++) {
-                if (dx == 0 && dy == 0) continue;
-                uint32_t v = sad_block(cur, ref, W, H, B, bx, by, dx, dy);
-                pts++;
-                if (v < best) { best = v; mx = dx; my = dy; }
-            }
-        }
-        if (mv_out) { mv_out[2 * i] = (int16_t)mx; mv_out[2 * i + 1] = (int16_t)my; }
-        if (sad_out) sad_out[i] = best;
-        if (points_out) points_out[i] = (uint16_t)pts;  /* (2p+1)^2 under C9 (225) */
-    }
+    for (int i = 0; i < nbx * nby; i++)
+        if (oracle_fullsearch_block(cur, ref, W, H, B, p, (i % nbx) * B, (i / nbx) * B,
+                                    mv_out + 2 * i, sad_out + i, points_out + i))
+            return -1;
     return 0;
 }
 

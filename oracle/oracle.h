@@ -50,6 +50,14 @@ int oracle_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int
 int oracle_fullsearch(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
                       int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out);
 
+/* Single-block versions (sampled parity at full size): block origin (bx,by). */
+int oracle_dcds_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
+                      int variant, int bx, int by, int16_t* mv_out, uint32_t* sad_out,
+                      uint16_t* points_out);
+int oracle_fullsearch_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
+                            int bx, int by, int16_t* mv_out, uint32_t* sad_out,
+                            uint16_t* points_out);
+
 /* Motion-compensated SSE and PSNR (P:342 aspect 4; reading C18):
  * pred(x,y) = R(x+mvx, y+mvy) for the block containing (x,y); SSE = sum (cur-pred)^2;
  * PSNR = 10*log10(255^2 * W*H / SSE), +inf when SSE == 0. */

@@ -1,0 +1,12 @@
+"""B200-native (sm_100a) DCDS block-motion-estimation hot path (Jia & Zhang, arxiv 0806.0689).
+
+The product is the C-ABI library ``libme.so`` (include/me.h) built from ``csrc/``;
+``me`` is its thin Python binding (marshalling only) and ``synth`` the seeded synthetic
+input generator.  There is no CPU fallback.
+"""
+from . import synth  # noqa: F401
+from .me import (  # noqa: F401
+    MEError, alloc_outputs, load, me_dcds, me_dcds_batch, me_dcds_batch_host, me_dcds_s_batch,
+    me_fullsearch, me_fullsearch_batch, me_init, me_launch_count, me_mc_psnr, me_mc_sse_batch,
+    me_set_stream, me_shutdown,
+)

@@ -1,0 +1,402 @@
+// me_api.cu -- C ABI of libme.so (include/me.h): validation, launch configuration, streams.
+//
+// Every entry point validates its arguments before any device work and launches the
+// sm_100a kernels of dcds_kernel.cuh / fs_kernel.cuh on the library stream.  There is no
+// CPU fallback: without a working sm_100 device every call fails with ME_ENOTINIT/ME_ECUDA.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "../../include/me.h"
+#include "dcds_kernel.cuh"
+#include "fs_kernel.cuh"
+
+namespace {
+
+int g_dev = -1;
+cudaStream_t g_stream = nullptr;
+cudaStream_t g_copy_streams[2] = {nullptr, nullptr};
+unsigned long long* g_scratch = nullptr;  // device u64 scratch (me_mc_psnr)
+char g_err[512] = "";
+long long g_launches = 0;
+int g_smem_optin = 0;
+
+// grow-only staging buffers of me_dcds_batch_host (two sets for double buffering)
+struct HostStage {
+    uint8_t* frames = nullptr;
+    size_t frames_cap = 0;
+    uint8_t* out = nullptr;
+    size_t out_cap = 0;
+};
+HostStage g_stage[2];
+
+constexpr int kNWarp = 8;
+
+int set_cuda_err(cudaError_t e, const char* where) {
+    snprintf(g_err, sizeof g_err, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+    return ME_ECUDA;
+}
+
+int fail(int code, const char* msg) {
+    snprintf(g_err, sizeof g_err, "%s", msg);
+    return code;
+}
+
+#define CK(call)                                               \
+    do {                                                       \
+        cudaError_t _e = (call);                               \
+        if (_e != cudaSuccess) return set_cuda_err(_e, #call); \
+    } while (0)
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool aligned(const void* p, unsigned a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+int validate_frames(const uint8_t* cur, const uint8_t* ref, long long stride, int npairs, int W,
+                    int H, int block) {
+    if (!cur || !ref) return fail(ME_EINVAL, "NULL frame pointer");
+    if (W <= 0 || H <= 0) return fail(ME_EINVAL, "W and H must be positive");
+    if (block != 8 && block != 16) return fail(ME_EINVAL, "block must be 8 or 16");
+    if (W % block || H % block) return fail(ME_EINVAL, "W and H must be multiples of block");
+    if (npairs < 1) return fail(ME_EINVAL, "npairs must be >= 1");
+    if (W > 32768 || H > 32768) return fail(ME_EINVAL, "frame larger than 32768");
+    if ((long long)(W / block) * (H / block) > (1ll << 31) / 4) return fail(ME_EINVAL, "too many blocks");
+    if (npairs > 65535) return fail(ME_EINVAL, "npairs must be <= 65535");
+    if (W % 16) return fail(ME_EALIGN, "W must be a multiple of 16");
+    if (!aligned16(cur) || !aligned16(ref)) return fail(ME_EALIGN, "frame pointers must be 16-byte aligned");
+    if (npairs > 1 && (stride % 16)) return fail(ME_EALIGN, "pair_stride must be a multiple of 16");
+    if (npairs > 1 && stride < (long long)W * H) return fail(ME_EINVAL, "pair_stride smaller than a frame");
+    return ME_OK;
+}
+
+int validate_search(const uint8_t* cur, const uint8_t* ref, long long stride, int npairs, int W,
+                    int H, int block, int p, const void* mv, const void* sad, const void* pts) {
+    int rc = validate_frames(cur, ref, stride, npairs, W, H, block);
+    if (rc) return rc;
+    if (p < 1 || p > 32) return fail(ME_EINVAL, "p must be in [1, 32]");
+    if (!mv || !sad || !pts) return fail(ME_EINVAL, "NULL output pointer");
+    if (!aligned(mv, 4) || !aligned(sad, 4) || !aligned(pts, 2))
+        return fail(ME_EALIGN, "output pointers must be naturally aligned (mv 4 B)");
+    return ME_OK;
+}
+
+struct DcdsLaunch {
+    me::SearchArgs a;
+    dim3 grid;
+    size_t smem;
+};
+
+DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
+    DcdsLaunch L;
+    me::SearchArgs& a = L.a;
+    const int nbx = W / B, nby = H / B;
+    int tbx = (B == 16) ? 8 : 16;
+    int tby = (B == 16) ? (p <= 8 ? 2 : 4) : (p <= 8 ? 4 : 8);
+    tbx = std::min(tbx, nbx);
+    tby = std::min(tby, nby);
+    const int TW = tbx * B, TH = tby * B;
+    a.W = W; a.H = H; a.p = p;
+    a.tbx = tbx; a.tby = tby;
+    a.ntx = (nbx + tbx - 1) / tbx;
+    const int nty = (nby + tby - 1) / tby;
+    // region width: x0 - xs <= p + 15, plus TW + p, plus 16 bytes of over-read slack
+    int pitch = ((TW + 2 * p + 31) + 15) & ~15;
+    if (((pitch >> 4) & 1) == 0) pitch += 16;  // 16 * odd: conflict-free rows for the B=16 engine
+    a.pitch = pitch;
+    a.rh = TH + 2 * p;
+    const int side = 2 * p + 1;
+    a.bm_words = (((side * side + 31) / 32) + 3) & ~3;
+    a.nbx = nbx;
+    a.nb = nbx * nby;
+    L.grid = dim3(a.ntx * nty, npairs);
+    L.smem = (size_t)pitch * a.rh + 16 + (size_t)TW * TH + (size_t)kNWarp * a.bm_words * 4 + 32;
+    return L;
+}
+
+template <int B, int VARIANT>
+void launch_dcds_t(const DcdsLaunch& L, cudaStream_t s) {
+    me::dcds_kernel<B, kNWarp, VARIANT><<<L.grid, kNWarp * 32, L.smem, s>>>(L.a);
+}
+
+int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W, int H,
+             int block, int p, int16_t* mv, uint32_t* sad, uint16_t* pts, uint64_t* stats,
+             int variant, cudaStream_t s) {
+    DcdsLaunch L = plan_dcds(W, H, block, p, npairs);
+    if ((int)L.smem > g_smem_optin) return fail(ME_EINVAL, "tile does not fit in shared memory");
+    L.a.cur0 = cur0; L.a.ref0 = ref0; L.a.stride = stride;
+    L.a.mv = reinterpret_cast<uint32_t*>(mv);
+    L.a.sad = sad;
+    L.a.pts = pts;
+    L.a.stats = reinterpret_cast<unsigned long long*>(stats);
+    if (stats) CK(cudaMemsetAsync(stats, 0, sizeof(uint64_t) * 3 * (size_t)npairs, s));
+    if (block == 16) {
+        if (variant) launch_dcds_t<16, 1>(L, s); else launch_dcds_t<16, 0>(L, s);
+    } else {
+        if (variant) launch_dcds_t<8, 1>(L, s); else launch_dcds_t<8, 0>(L, s);
+    }
+    g_launches++;
+    CK(cudaGetLastError());
+    return ME_OK;
+}
+
+int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W, int H,
+           int block, int p, int16_t* mv, uint32_t* sad, uint16_t* pts, uint64_t* stats,
+           cudaStream_t s) {
+    me::FsArgs a;
+    a.cur0 = cur0; a.ref0 = ref0; a.stride = stride;
+    a.W = W; a.H = H; a.p = p;
+    a.nbx = W / block; a.nb = a.nbx * (H / block);
+    a.lw = ((2 * p) >> 2) + block / 4 + 1;
+    a.mv = reinterpret_cast<uint32_t*>(mv); a.sad = sad; a.pts = pts;
+    a.stats = reinterpret_cast<unsigned long long*>(stats);
+    const size_t smem = (size_t)4 * (block + 2 * p) * a.lw * 4 + (size_t)block * block;
+    if ((int)smem > g_smem_optin) return fail(ME_EINVAL, "FS window does not fit in shared memory");
+    if (stats) CK(cudaMemsetAsync(stats, 0, sizeof(uint64_t) * 3 * (size_t)npairs, s));
+    dim3 grid(a.nb, npairs);
+    if (block == 16) me::fs_kernel<16><<<grid, 256, smem, s>>>(a);
+    else me::fs_kernel<8><<<grid, 256, smem, s>>>(a);
+    g_launches++;
+    CK(cudaGetLastError());
+    return ME_OK;
+}
+
+int run_mc_sse(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W,
+               int H, int block, const int16_t* mv, uint64_t* sse, cudaStream_t s) {
+    me::McArgs a;
+    a.cur0 = cur0; a.ref0 = ref0; a.stride = stride;
+    a.W = W; a.H = H; a.B = block;
+    a.nbx = W / block; a.nb = a.nbx * (H / block);
+    a.mv = reinterpret_cast<const uint32_t*>(mv);
+    a.sse = reinterpret_cast<unsigned long long*>(sse);
+    CK(cudaMemsetAsync(sse, 0, sizeof(uint64_t) * (size_t)npairs, s));
+    dim3 grid((a.nb + 7) / 8, npairs);
+    me::mc_sse_kernel<<<grid, 256, 0, s>>>(a);
+    g_launches++;
+    CK(cudaGetLastError());
+    return ME_OK;
+}
+
+template <typename K>
+int allow_smem(K kernel) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin));
+    return ME_OK;
+}
+
+int grow(uint8_t** p, size_t* cap, size_t need) {
+    if (*cap >= need) return ME_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    if (cudaMalloc(p, need) != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return fail(ME_ENOMEM, "staging buffer allocation failed");
+    }
+    *cap = need;
+    return ME_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int me_init(int device) {
+    if (g_dev == device) return ME_OK;
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return fail(ME_EINVAL, "no such CUDA device");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        snprintf(g_err, sizeof g_err, "device %d is sm_%d%d; libme.so is built for sm_100a only",
+                 device, prop.major, prop.minor);
+        return ME_ECUDA;
+    }
+    g_smem_optin = (int)prop.sharedMemPerBlockOptin;
+    int rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, kNWarp, 0>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, kNWarp, 1>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, kNWarp, 0>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, kNWarp, 1>))) return rc;
+    if ((rc = allow_smem(me::fs_kernel<16>))) return rc;
+    if ((rc = allow_smem(me::fs_kernel<8>))) return rc;
+    if (!g_scratch) CK(cudaMalloc(&g_scratch, 64));
+    for (auto& cs : g_copy_streams)
+        if (!cs) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    g_dev = device;
+    g_launches = 0;
+    return ME_OK;
+}
+
+int me_set_stream(void* stream) {
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    g_stream = reinterpret_cast<cudaStream_t>(stream);
+    return ME_OK;
+}
+
+int me_dcds_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs, int W,
+                  int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
+                  uint16_t* points_out, uint64_t* stats_out) {
+    int rc = validate_search(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out,
+                             points_out);
+    if (rc) return rc;
+    if (stats_out && !aligned(stats_out, 8)) return fail(ME_EALIGN, "stats_out must be 8-byte aligned");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    return run_dcds(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
+                    stats_out, 0, g_stream);
+}
+
+int me_dcds_s_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                    int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
+                    uint16_t* points_out, uint64_t* stats_out) {
+    int rc = validate_search(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out,
+                             points_out);
+    if (rc) return rc;
+    if (stats_out && !aligned(stats_out, 8)) return fail(ME_EALIGN, "stats_out must be 8-byte aligned");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    return run_dcds(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
+                    stats_out, 1, g_stream);
+}
+
+int me_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int block, int p,
+            int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out) {
+    return me_dcds_batch(cur, ref, 0, 1, W, H, block, p, mv_out, sad_out, points_out, nullptr);
+}
+
+int me_fullsearch_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                        int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
+                        uint16_t* points_out, uint64_t* stats_out) {
+    int rc = validate_search(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out,
+                             points_out);
+    if (rc) return rc;
+    if (stats_out && !aligned(stats_out, 8)) return fail(ME_EALIGN, "stats_out must be 8-byte aligned");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    return run_fs(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
+                  stats_out, g_stream);
+}
+
+int me_fullsearch(const uint8_t* cur, const uint8_t* ref, int W, int H, int block, int p,
+                  int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out) {
+    return me_fullsearch_batch(cur, ref, 0, 1, W, H, block, p, mv_out, sad_out, points_out,
+                               nullptr);
+}
+
+int me_mc_sse_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                    int W, int H, int block, const int16_t* mv, uint64_t* sse_out) {
+    int rc = validate_frames(cur0, ref0, pair_stride, npairs, W, H, block);
+    if (rc) return rc;
+    if (!mv || !sse_out) return fail(ME_EINVAL, "NULL mv / sse pointer");
+    if (!aligned(mv, 4) || !aligned(sse_out, 8)) return fail(ME_EALIGN, "mv / sse_out misaligned");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    return run_mc_sse(cur0, ref0, pair_stride, npairs, W, H, block, mv, sse_out, g_stream);
+}
+
+int me_mc_psnr(const uint8_t* cur, const uint8_t* ref, int W, int H, int block, const int16_t* mv,
+               double* psnr_out, uint64_t* sse_out) {
+    int rc = validate_frames(cur, ref, 0, 1, W, H, block);
+    if (rc) return rc;
+    if (!mv || !psnr_out) return fail(ME_EINVAL, "NULL mv / psnr pointer");
+    if (!aligned(mv, 4)) return fail(ME_EALIGN, "mv must be 4-byte aligned");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    rc = run_mc_sse(cur, ref, 0, 1, W, H, block, mv, reinterpret_cast<uint64_t*>(g_scratch), g_stream);
+    if (rc) return rc;
+    unsigned long long sse = 0;
+    CK(cudaMemcpyAsync(&sse, g_scratch, sizeof sse, cudaMemcpyDeviceToHost, g_stream));
+    CK(cudaStreamSynchronize(g_stream));
+    if (sse_out) *sse_out = sse;
+    // PSNR of the compensated frame (P:342 aspect 4; reading C18)
+    *psnr_out = sse == 0 ? INFINITY : 10.0 * log10((255.0 * 255.0) * ((double)W * H) / (double)sse);
+    return ME_OK;
+}
+
+int me_dcds_batch_host(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                       int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
+                       uint16_t* points_out, uint64_t* stats_out) {
+    if (!cur0 || !ref0) return fail(ME_EINVAL, "NULL frame pointer");
+    if (npairs > 1 && pair_stride < (long long)W * H) return fail(ME_EINVAL, "pair_stride smaller than a frame");
+    const long long span0 = std::llabs((long long)(ref0 - cur0)) + (long long)W * H;  // one pair
+    if (npairs > 1 && span0 > pair_stride) return fail(ME_EINVAL, "cur/ref of a pair must lie within pair_stride");
+    // host pointers: alignment of the device staging copy is what the kernels need
+    int rc = validate_search(reinterpret_cast<const uint8_t*>(16), reinterpret_cast<const uint8_t*>(16),
+                             pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out);
+    if (rc) return rc;
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    if ((std::llabs((long long)(ref0 - cur0)) & 15) != 0)
+        return fail(ME_EALIGN, "ref0 - cur0 must be a multiple of 16 bytes");
+    const uint8_t* hbase = std::min(cur0, ref0);
+    const long long cur_off = cur0 - hbase, ref_off = ref0 - hbase;
+    const long long stride = npairs > 1 ? pair_stride : ((span0 + 15) & ~15ll);
+    const int nb = (W / block) * (H / block);
+    // chunk: ~256 MiB of frames per buffer
+    int chunk = (int)std::max(1ll, std::min<long long>(npairs, (256ll << 20) / stride));
+    const size_t fbytes = (size_t)stride * chunk;
+    const size_t obytes = (size_t)chunk * nb * (4 + 4 + 2) + (size_t)chunk * 24 + 64;
+    for (auto& st : g_stage) {
+        if ((rc = grow(&st.frames, &st.frames_cap, fbytes))) return rc;
+        if ((rc = grow(&st.out, &st.out_cap, obytes))) return rc;
+    }
+    // order the copies after whatever the caller queued on the library stream
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, g_stream));
+    for (auto cs : g_copy_streams) CK(cudaStreamWaitEvent(cs, ev, 0));
+    CK(cudaEventDestroy(ev));
+    for (int c0 = 0, ci = 0; c0 < npairs; c0 += chunk, ci++) {
+        const int n = std::min(chunk, npairs - c0);
+        HostStage& st = g_stage[ci & 1];
+        cudaStream_t s = g_copy_streams[ci & 1];
+        const size_t bytes = (size_t)(n - 1) * stride + (size_t)span0;
+        CK(cudaMemcpyAsync(st.frames, hbase + (size_t)c0 * stride, bytes, cudaMemcpyHostToDevice, s));
+        int16_t* dmv = reinterpret_cast<int16_t*>(st.out);
+        uint32_t* dsad = reinterpret_cast<uint32_t*>(st.out + (size_t)n * nb * 4);
+        uint64_t* dst = reinterpret_cast<uint64_t*>(st.out + (((size_t)n * nb * 8 + 7) & ~(size_t)7));
+        uint16_t* dpts = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(dst) + (size_t)n * 24);
+        rc = run_dcds(st.frames + cur_off, st.frames + ref_off, stride, n, W, H, block, p, dmv,
+                      dsad, dpts, dst, 0, s);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(mv_out + (size_t)c0 * nb * 2, dmv, (size_t)n * nb * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(sad_out + (size_t)c0 * nb, dsad, (size_t)n * nb * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(points_out + (size_t)c0 * nb, dpts, (size_t)n * nb * 2, cudaMemcpyDeviceToHost, s));
+        if (stats_out)
+            CK(cudaMemcpyAsync(stats_out + (size_t)c0 * 3, dst, (size_t)n * 24, cudaMemcpyDeviceToHost, s));
+    }
+    for (auto cs : g_copy_streams) CK(cudaStreamSynchronize(cs));
+    return ME_OK;
+}
+
+int64_t me_launch_count(void) { return g_launches; }
+
+const char* me_strerror(int status) {
+    switch (status) {
+        case ME_OK: return "ok";
+        case ME_EINVAL: return g_err[0] ? g_err : "invalid argument";
+        case ME_EALIGN: return g_err[0] ? g_err : "misaligned argument";
+        case ME_ENOTINIT: return "me_init has not succeeded";
+        case ME_ECUDA: return g_err[0] ? g_err : "CUDA error";
+        case ME_ENOMEM: return g_err[0] ? g_err : "out of device memory";
+        default: return "unknown status";
+    }
+}
+
+void me_shutdown(void) {
+    if (g_dev < 0) return;
+    for (auto& st : g_stage) {
+        if (st.frames) cudaFree(st.frames);
+        if (st.out) cudaFree(st.out);
+        st = HostStage();
+    }
+    if (g_scratch) cudaFree(g_scratch);
+    g_scratch = nullptr;
+    for (auto& cs : g_copy_streams) {
+        if (cs) cudaStreamDestroy(cs);
+        cs = nullptr;
+    }
+    g_stream = nullptr;
+    g_dev = -1;
+}
+
+}  // extern "C"

@@ -1,0 +1,277 @@
+"""GPU parity: libme.so (sm_100a) against the CPU oracle, through the C ABI.
+
+Integer outputs (mv, SAD, points, SSE) must be bit-identical; PSNR within 1e-9 dB
+(BASELINE.json north_star).  Sizes span several tiles with ragged tails; the full-size
+configs c3/c4 run in the bench's launch configuration (one batched launch over all pairs)
+and are checked on whole sampled pairs plus sampled blocks the oracle computes one by one.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_0806_0689_b200 as me
+from paper_0806_0689_b200 import synth
+from _golden import golden_matrix
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
+
+
+@pytest.fixture(scope="module", autouse=True)
+def init():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    me.me_init(0)
+    me.me_set_stream(torch.cuda.current_stream())
+    yield
+
+
+def to_np(t):
+    return t.cpu().numpy()
+
+
+def gpu_search(frames, B, p, kind="dcds"):
+    n, _, H, W = frames.shape
+    nb = (W // B) * (H // B)
+    mv, sad, pts, st = me.alloc_outputs(n, nb, frames.device)
+    fn = {"dcds": me.me_dcds_batch, "dcds_s": me.me_dcds_s_batch, "fs": me.me_fullsearch_batch}[kind]
+    fn(frames, B, p, mv, sad, pts, st)
+    torch.cuda.synchronize()
+    return (to_np(mv), to_np(sad).astype(np.uint32), to_np(pts).astype(np.uint16),
+            to_np(st).astype(np.uint64))
+
+
+def assert_pair_equal(host_pair, B, p, mv, sad, pts, kind="dcds", tag=""):
+    cur, ref = host_pair[0], host_pair[1]
+    if kind == "fs":
+        omv, osad, opts = oracle.fullsearch(cur, ref, B, p)
+    else:
+        omv, osad, opts = oracle.dcds(cur, ref, B, p, 1 if kind == "dcds_s" else 0)
+    bad = np.flatnonzero((mv != omv).any(1) | (sad != osad) | (pts != opts))
+    assert bad.size == 0, (f"{tag} {kind} B={B} p={p}: {bad.size} blocks differ, first {bad[:5]}: "
+                           f"gpu {mv[bad[0]]},{sad[bad[0]]},{pts[bad[0]]} "
+                           f"oracle {omv[bad[0]]},{osad[bad[0]]},{opts[bad[0]]}")
+    return omv, osad, opts
+
+
+def frames_from_np(cur, ref):
+    return torch.from_numpy(np.stack([cur, ref])[None].copy()).to(DEV)
+
+
+# ---------------------------------------------------------------------------------------
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()
+
+
+def test_c0_c1_all_pairs_dcds_fs_psnr():
+    for name in ("c0", "c1"):
+        cfg = synth.CONFIGS[name]
+        fr = synth.make_sequence(cfg, device=DEV)
+        host = to_np(fr)
+        mv, sad, pts, st = gpu_search(fr, cfg.B, cfg.p)
+        fmv, fsad, fpts, fst = gpu_search(fr, cfg.B, cfg.p, "fs")
+        sse_dev = torch.empty(cfg.npairs, dtype=torch.int64, device=DEV)
+        me.me_mc_sse_batch(fr, cfg.B, torch.from_numpy(mv).to(DEV), sse_dev)
+        sse_dev = to_np(sse_dev)
+        for t in range(cfg.npairs):
+            omv, osad, opts = assert_pair_equal(host[t], cfg.B, cfg.p, mv[t], sad[t], pts[t], tag=f"{name}/{t}")
+            assert_pair_equal(host[t], cfg.B, cfg.p, fmv[t], fsad[t], fpts[t], "fs", tag=f"{name}/{t}")
+            ops, osse = oracle.mc_psnr(host[t, 0], host[t, 1], cfg.B, omv)
+            assert st[t].tolist() == [int(opts.sum()), int(osad.sum()), osse]
+            assert int(sse_dev[t]) == osse
+            ps, sse = me.me_mc_psnr(fr[t, 0], fr[t, 1], cfg.B, torch.from_numpy(mv[t]).to(DEV))
+            assert sse == osse and abs(ps - ops) <= 1e-9
+            fo = oracle.fullsearch(host[t, 0], host[t, 1], cfg.B, cfg.p)
+            assert fst[t].tolist() == [int(fo[2].astype(np.int64).sum()), int(fo[1].astype(np.int64).sum()),
+                                       oracle.mc_psnr(host[t, 0], host[t, 1], cfg.B, fo[0])[1]]
+            assert (fsad[t] <= sad[t]).all()
+
+
+def test_c2_pairs():
+    cfg = synth.CONFIGS["c2"]
+    pairs = list(range(1, 300, 13))
+    fr = synth.make_sequence(cfg, device=DEV, pairs=pairs)
+    host = to_np(fr)
+    mv, sad, pts, st = gpu_search(fr, cfg.B, cfg.p)
+    for k in range(len(pairs)):
+        assert_pair_equal(host[k], cfg.B, cfg.p, mv[k], sad[k], pts[k], tag=f"c2/{pairs[k]}")
+    fmv, fsad, fpts, _ = gpu_search(fr[:3].contiguous(), cfg.B, cfg.p, "fs")
+    for k in range(3):
+        assert_pair_equal(host[k], cfg.B, cfg.p, fmv[k], fsad[k], fpts[k], "fs", tag=f"c2/{pairs[k]}")
+
+
+def _sampled_full_size(name, n_full, n_blocks, fs_pairs, seed):
+    """Full sequence on the GPU in one batched launch (the bench's configuration); whole
+    pairs and random blocks checked against the oracle; stats checked against the outputs
+    at every pair (a property that holds at any size)."""
+    cfg = synth.CONFIGS[name]
+    fr = synth.make_sequence(cfg, device=DEV)
+    mv, sad, pts, st = gpu_search(fr, cfg.B, cfg.p)
+    # stats == sums of the per-block outputs, every pair
+    np.testing.assert_array_equal(st[:, 0], pts.astype(np.int64).sum(1))
+    np.testing.assert_array_equal(st[:, 1], sad.astype(np.int64).sum(1))
+    sse_dev = torch.empty(cfg.npairs, dtype=torch.int64, device=DEV)
+    me.me_mc_sse_batch(fr, cfg.B, torch.from_numpy(mv).to(DEV), sse_dev)
+    np.testing.assert_array_equal(st[:, 2], to_np(sse_dev))
+    assert (pts >= 7).all()   # border blocks too (reading C9), p >= 2
+    rng = np.random.default_rng(seed)
+    full = sorted(set([0, cfg.npairs - 1] + list(rng.integers(0, cfg.npairs, n_full - 2))))
+    for t in full:
+        host = to_np(fr[t])
+        omv, osad, opts = assert_pair_equal(host, cfg.B, cfg.p, mv[t], sad[t], pts[t], tag=f"{name}/{t}")
+        assert int(st[t, 2]) == oracle.mc_psnr(host[0], host[1], cfg.B, omv)[1]
+    nbx = cfg.W // cfg.B
+    ts = rng.integers(0, cfg.npairs, n_blocks)
+    bs = rng.integers(0, cfg.nb, n_blocks)
+    cache = {}
+    for t, b in zip(ts, bs):
+        if t not in cache:
+            cache[t] = to_np(fr[t])
+        host = cache[t]
+        bx, by = (b % nbx) * cfg.B, (b // nbx) * cfg.B
+        omv, osad, opts = oracle.dcds_block(host[0], host[1], cfg.B, cfg.p, bx, by)
+        assert (tuple(mv[t, b]), sad[t, b], pts[t, b]) == (omv, osad, opts), (t, b)
+    # FS on a few pairs, sampled blocks (the oracle FS is (2p+1)^2 B^2 per block)
+    fsel = fr[fs_pairs].contiguous()
+    fmv, fsad, fpts, _ = gpu_search(fsel, cfg.B, cfg.p, "fs")
+    for k, t in enumerate(fs_pairs):
+        host = to_np(fr[t])
+        for b in list(rng.integers(0, cfg.nb, 40)) + [0, nbx - 1, cfg.nb - nbx, cfg.nb - 1]:
+            bx, by = (b % nbx) * cfg.B, (b // nbx) * cfg.B
+            omv, osad, opts = oracle.fullsearch_block(host[0], host[1], cfg.B, cfg.p, bx, by)
+            assert (tuple(fmv[k, b]), fsad[k, b], fpts[k, b]) == (omv, osad, opts), (t, b)
+            assert fsad[k, b] <= sad[t, b]
+    del fr
+    torch.cuda.empty_cache()
+
+
+def test_c3_full_size_sampled():
+    _sampled_full_size("c3", 4, 3000, [0, 118], seed=3)
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled():
+    _sampled_full_size("c4", 2, 1000, [0], seed=4)
+
+
+@pytest.mark.parametrize("B", [16, 8])
+def test_ideal_mosaic_table7(B):
+    """Pixel-ideal mosaic (SAD = B|q-t|^2 + K): the GPU kernel reproduces Table VII
+     and the full ideal NSP map, with the true MV everywhere."""
+    cur, ref, tile, off, blocks = synth.ideal_mosaic(B, 7)
+    mv, sad, pts, _ = gpu_search(frames_from_np(cur, ref), B, 7)
+    got = pts[0][blocks]
+    np.testing.assert_array_equal(got[7:, 7:], golden_matrix("table7_dcds.txt", int))
+    nsp, mx, my = oracle.ideal_nsp_map(7)
+    np.testing.assert_array_equal(got, nsp)
+    np.testing.assert_array_equal(mv[0][blocks][..., 0], mx)
+    np.testing.assert_array_equal(mv[0][blocks][..., 1], my)
+    assert_pair_equal(np.stack([cur, ref]), B, 7, mv[0], sad[0], pts[0], tag="mosaic")
+
+
+SPECIAL = [
+    ("flat", 176, 144), ("binary", 176, 144), ("random", 176, 144), ("texture", 176, 144),
+    ("border16", 48, 48), ("border8", 32, 24), ("tiny", 16, 16), ("wide", 400, 32),
+]
+
+
+def special_pair(kind, W, H, seed=0):
+    if kind == "flat":
+        return synth.flat_pair(W, H, 77)
+    if kind == "binary":
+        return synth.binary_pair(W, H, seed + 1)
+    if kind == "texture":
+        tex = synth.texture(W, H, (2.0,), seed + 2).numpy()
+        return synth.translated_pair(tex, 3, -1)
+    return synth.random_pair(W, H, seed + 3)
+
+
+@pytest.mark.parametrize("kind,W,H", SPECIAL)
+@pytest.mark.parametrize("B", [16, 8])
+@pytest.mark.parametrize("p", [1, 2, 7, 15, 16, 32])
+def test_special_inputs(kind, W, H, B, p):
+    if W % B or H % B:
+        pytest.skip("frame not divisible by block")
+    cur, ref = special_pair(kind, W, H, seed=p * 3 + B)
+    fr = frames_from_np(cur, ref)
+    host = np.stack([cur, ref])
+    for k in ("dcds", "dcds_s"):
+        mv, sad, pts, st = gpu_search(fr, B, p, k)
+        assert_pair_equal(host, B, p, mv[0], sad[0], pts[0], k, tag=kind)
+    if p <= 16 or W * H <= 48 * 48:
+        mv, sad, pts, st = gpu_search(fr, B, p, "fs")
+        assert_pair_equal(host, B, p, mv[0], sad[0], pts[0], "fs", tag=kind)
+
+
+def test_dcds_s_c1():
+    cfg = synth.CONFIGS["c1"]
+    fr = synth.make_sequence(cfg, device=DEV, pairs=range(1, 12))
+    host = to_np(fr)
+    mv, sad, pts, _ = gpu_search(fr, cfg.B, cfg.p, "dcds_s")
+    dmv, dsad, dpts, _ = gpu_search(fr, cfg.B, cfg.p, "dcds")
+    for t in range(fr.shape[0]):
+        assert_pair_equal(host[t], cfg.B, cfg.p, mv[t], sad[t], pts[t], "dcds_s")
+    assert (pts <= dpts).all()
+
+
+def test_single_pair_entry_points():
+    cfg = synth.CONFIGS["c0"]
+    fr = synth.make_sequence(cfg, device=DEV)
+    cur, ref = fr[0, 0], fr[0, 1]
+    mv = torch.empty(cfg.nb, 2, dtype=torch.int16, device=DEV)
+    sad = torch.empty(cfg.nb, dtype=torch.int32, device=DEV)
+    pts = torch.empty(cfg.nb, dtype=torch.int16, device=DEV)
+    me.me_dcds(cur, ref, cfg.B, cfg.p, mv, sad, pts)
+    torch.cuda.synchronize()
+    host = to_np(fr[0])
+    assert_pair_equal(host, cfg.B, cfg.p, to_np(mv), to_np(sad).astype(np.uint32),
+                      to_np(pts).astype(np.uint16))
+    me.me_fullsearch(cur, ref, cfg.B, cfg.p, mv, sad, pts)
+    torch.cuda.synchronize()
+    assert_pair_equal(host, cfg.B, cfg.p, to_np(mv), to_np(sad).astype(np.uint32),
+                      to_np(pts).astype(np.uint16), "fs")
+    ps, sse = me.me_mc_psnr(ref, ref, cfg.B, torch.zeros(cfg.nb, 2, dtype=torch.int16, device=DEV))
+    assert sse == 0 and math.isinf(ps)
+
+
+def test_host_buffer_variant_matches_device():
+    cfg = synth.CONFIGS["c1"]
+    fr = synth.make_sequence(cfg, device=DEV)
+    mv, sad, pts, st = gpu_search(fr, cfg.B, cfg.p)
+    hfr = fr.cpu().pin_memory()
+    hmv, hsad, hpts, hst = me.alloc_outputs(cfg.npairs, cfg.nb, "cpu")
+    me.me_dcds_batch_host(hfr, cfg.B, cfg.p, hmv, hsad, hpts, hst)
+    np.testing.assert_array_equal(hmv.numpy(), mv)
+    np.testing.assert_array_equal(hsad.numpy().astype(np.uint32), sad)
+    np.testing.assert_array_equal(hpts.numpy().astype(np.uint16), pts)
+    np.testing.assert_array_equal(hst.numpy().astype(np.uint64), st)
+
+
+def test_user_stream_and_launch_count():
+    cfg = synth.CONFIGS["c1"]
+    fr = synth.make_sequence(cfg, device=DEV, pairs=[1, 2])
+    s = torch.cuda.Stream()
+    n0 = me.me_launch_count()
+    with torch.cuda.stream(s):
+        me.me_set_stream(s)
+        out = me.alloc_outputs(2, cfg.nb, DEV)
+        me.me_dcds_batch(fr, cfg.B, cfg.p, *out)
+    s.synchronize()
+    me.me_set_stream(torch.cuda.current_stream())
+    assert me.me_launch_count() == n0 + 1
+    ref = gpu_search(fr, cfg.B, cfg.p)
+    np.testing.assert_array_equal(to_np(out[0]), ref[0])
+
+
+def test_errors_raise():
+    fr = torch.zeros(1, 2, 32, 40, dtype=torch.uint8, device=DEV)
+    out = me.alloc_outputs(1, 20, DEV)
+    with pytest.raises(me.MEError):
+        me.me_dcds_batch(fr, 16, 7, *out)     # 40 % 16 != 0
