@@ -153,7 +153,7 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
     a.mv = reinterpret_cast<uint32_t*>(mv); a.sad = sad; a.pts = pts;
     a.stats = reinterpret_cast<unsigned long long*>(stats);
     const size_t smem = (size_t)4 * (block + 2 * p) * a.lw * 4 + (size_t)block * block;
-    if ((int)smem > g_smem_optin) return fail(ME_EINVAL, "FS window does not fit in shared memory");
+    if ((int)smem > g_smem_optin - 64) return fail(ME_EINVAL, "FS window does not fit in shared memory");
     if (stats) CK(cudaMemsetAsync(stats, 0, sizeof(uint64_t) * 3 * (size_t)npairs, s));
     dim3 grid(a.nb, npairs);
     if (block == 16) me::fs_kernel<16><<<grid, 256, smem, s>>>(a);
@@ -181,7 +181,10 @@ int run_mc_sse(const uint8_t* cur0, const uint8_t* ref0, long long stride, int n
 
 template <typename K>
 int allow_smem(K kernel) {
-    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, kernel));
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            g_smem_optin - (int)fa.sharedSizeBytes));
     return ME_OK;
 }
 

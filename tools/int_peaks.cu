@@ -20,6 +20,12 @@ __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <int OP>
 __global__ void kern(uint32_t* out, int iters, uint32_t seed, long long* cycles) {
     uint32_t acc[NCHAIN];
@@ -27,6 +33,7 @@ __global__ void kern(uint32_t* out, int iters, uint32_t seed, long long* cycles)
 #pragma unroll
     for (int k = 0; k < NCHAIN; k++) acc[k] = a + k;
     long long t0 = clock64();
+    unsigned long long g0 = gtimer();
     for (int i = 0; i < iters; i++) {
 #pragma unroll
         for (int k = 0; k < NCHAIN; k++) {
@@ -37,11 +44,12 @@ __global__ void kern(uint32_t* out, int iters, uint32_t seed, long long* cycles)
         }
     }
     long long t1 = clock64();
+    unsigned long long g1 = gtimer();
     uint32_t s = 0;
 #pragma unroll
     for (int k = 0; k < NCHAIN; k++) s ^= acc[k];
     if (s == 0x12345678u) out[0] = s;
-    if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = t1 - t0;
+    if (threadIdx.x == 0 && blockIdx.x == 0) { cycles[0] = t1 - t0; cycles[1] = (long long)(g1 - g0); }
 }
 
 template <int OP>
@@ -49,7 +57,7 @@ double run(const char* name, int sms, int blocks_per_sm, int threads, int iters,
     uint32_t* out;
     long long* cyc;
     cudaMalloc(&out, 4);
-    cudaMalloc(&cyc, 8);
+    cudaMalloc(&cyc, 16);
     dim3 grid(sms * blocks_per_sm);
     kern<OP><<<grid, threads>>>(out, iters / 10, 1u, cyc);  // warm-up
     cudaDeviceSynchronize();
@@ -62,12 +70,12 @@ double run(const char* name, int sms, int blocks_per_sm, int threads, int iters,
     cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
-    long long c = 0;
-    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    long long c[2] = {0, 1};
+    cudaMemcpy(c, cyc, 16, cudaMemcpyDeviceToHost);
     const double lane_ops = (double)grid.x * threads * iters * NCHAIN;
     const double per_s = lane_ops / (ms * 1e-3);
-    const double clk_hz = (double)c / (ms * 1e-3);  // SM clock seen by block 0 over the kernel
-    *ops_per_sm_clk = lane_ops / ((double)c * sms);
+    const double clk_hz = (double)c[0] / ((double)c[1] * 1e-9);  // block 0: cycles / ns
+    *ops_per_sm_clk = per_s / (clk_hz * sms);
     printf("  \"%s\": {\"lane_ops_per_s\": %.6e, \"ms\": %.3f, \"sm_clock_mhz_est\": %.1f, "
            "\"lane_ops_per_sm_per_clk\": %.3f},\n",
            name, per_s, ms, clk_hz / 1e6, *ops_per_sm_clk);
