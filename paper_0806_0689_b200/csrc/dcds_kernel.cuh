@@ -14,12 +14,18 @@
 //
 // Design: one CTA per tile of TBX x TBY blocks of one pair; the tile's
 // reference region (tile + the whole +-p window, edge-replicated) and current tile are staged
-// once into shared memory; each warp then runs DCDS for one block at a time (blocks handed
-// out by a shared counter).  Inside a warp, lanes split the block's rows (and, for 8x8
-// blocks, four candidate slots); SADs use VABSDIFF4 (inline PTX vabsdiff4.add), warp sums
-// use REDUX.SUM, argmins are packed integer keys, and the visited set is a per-warp bitmap in
-// shared memory.  The data-dependent step count runs inside the warp with no block/grid sync.
+// once into shared memory.  Each warp is split into 32/G lane groups; each group runs DCDS
+// on one block at a time (G lanes split the block's rows), so a warp carries 32/G blocks.
+// The search is a per-group state machine (S1a, S1b = the 7 HCSP points in two passes of 4
+// slots; S3 = the 4 DDSP points; S4 = the middle points) advanced one pass per warp
+// iteration, so groups at different steps share one instruction stream and the
+// data-dependent step count never needs a block or grid sync.  A group that finishes takes
+// the next block of the tile from a shared counter.  SADs use VABSDIFF4 (inline PTX
+// vabsdiff4.add) on funnel-shifted unaligned rows; the 4 slot sums are packed two per word
+// (each <= 255*B*B < 2^16) and reduced across the group with xor shuffles; argmins are
+// packed (SAD, order) keys; the visited set is a per-group bitmap in shared memory.
 #pragma once
+#include <cuda.h>  // CUtensorMap
 #include <stdint.h>
 
 namespace me {
@@ -33,12 +39,14 @@ struct SearchArgs {
     int W, H, p;
     int tbx, tby, ntx;      // tile size in blocks; tiles per row
     int pitch, rh;          // staged reference region: row pitch (bytes, 16*odd) and rows
+    int cur_off;            // byte offset of the current tile in shared memory (128-aligned)
     int bm_words;           // visited-bitmap words per warp (multiple of 4)
     int nbx, nb;            // blocks per row, blocks per pair
     uint32_t* mv;           // [npairs][nb] packed (dx & 0xffff) | (dy << 16)
     uint32_t* sad;          // [npairs][nb]
     uint16_t* pts;          // [npairs][nb]
     unsigned long long* stats;  // [npairs][3] or null
+    uint32_t pcode[8];          // pattern code words (pat_code), see below
 };
 
 __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
@@ -60,32 +68,79 @@ __device__ __forceinline__ uint32_t lds_u8x4(const uint32_t* s, int o) {
 
 // Stage the reference region [ys, ys+rh) x [xs, xs+pitch) with edge replication, and the
 // current tile [y0, y0+TH) x [x0, x0+TW) (in-frame part), 16 bytes per thread-iteration.
-__device__ __forceinline__ void stage_tile(const SearchArgs& a, const uint8_t* cur,
-                                           const uint8_t* ref, int xs, int ys, int x0, int y0,
-                                           int TW, int TH, uint8_t* sref, uint8_t* scur) {
-    const int cpr = a.pitch >> 4;
-    for (int c = threadIdx.x; c < cpr * a.rh; c += blockDim.x) {
-        const int i = c / cpr, j = c - i * cpr;
-        const int y = min(max(ys + i, 0), a.H - 1);
-        const int x = xs + 16 * j;
-        const uint8_t* row = ref + (long long)y * a.W;
-        uint4 v;
-        if (x >= 0 && x < a.W) {
-            v = __ldg(reinterpret_cast<const uint4*>(row + x));
-        } else {
-            uint32_t b = (x < 0) ? row[0] : row[a.W - 1];
-            b *= 0x01010101u;
-            v = make_uint4(b, b, b, b);
+// ---- TMA / mbarrier helpers (sm_90+ PTX; SASS: UTMALDG, SYNCS.*) ---------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+}
+// 3-D tiled TMA load (x, y, pair) -> shared; out-of-bounds elements are zero-filled.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Edge replication (reading C9) of a TMA-staged region whose box reached outside the frame
+// (TMA zero-fills there).  Region rows i <-> frame row ys+i, columns c <-> frame column xs+c.
+// Phase A replicates the edge column into out-of-frame columns of every in-frame row; phase B
+// copies the nearest in-frame row into out-of-frame rows.  Border tiles only.
+__device__ __forceinline__ void fixup_edges(uint8_t* sref, int pitch, int rh, int xs, int ys,
+                                            int W, int H) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int i0 = max(0, -ys), i1 = min(rh, H - ys);      // in-frame rows [i0, i1)
+    const int cl = max(0, -xs), cr = min(pitch, W - xs);    // in-frame cols [cl, cr)
+    if (cl > 0 || cr < pitch) {
+        for (int i = i0 + warp; i < i1; i += nw) {
+            uint8_t* row = sref + i * pitch;
+            const uint8_t vl = row[cl], vr = row[cr - 1];
+            for (int c = lane; c < cl; c += 32) row[c] = vl;
+            for (int c = cr + lane; c < pitch; c += 32) row[c] = vr;
         }
-        *reinterpret_cast<uint4*>(sref + i * a.pitch + 16 * j) = v;
     }
-    const int ccr = TW >> 4;
-    for (int c = threadIdx.x; c < ccr * TH; c += blockDim.x) {
-        const int i = c / ccr, j = c - i * ccr;
-        const int y = y0 + i, x = x0 + 16 * j;
-        if (y < a.H && x < a.W)
-            *reinterpret_cast<uint4*>(scur + i * TW + 16 * j) =
-                __ldg(reinterpret_cast<const uint4*>(cur + (long long)y * a.W + x));
+    __syncthreads();
+    if (i0 > 0 || i1 < rh) {
+        const int n16 = pitch >> 4;
+        for (int e = threadIdx.x; e < rh * n16; e += blockDim.x) {
+            const int i = e / n16, q = e - i * n16;
+            if (i >= i0 && i < i1) continue;
+            const int src = i < i0 ? i0 : i1 - 1;
+            reinterpret_cast<uint4*>(sref + i * pitch)[q] = reinterpret_cast<const uint4*>(sref + src * pitch)[q];
+        }
+    }
+}
+
+// R rows x W4 words of the reference at byte offset o of the staged region (funnel-shifted
+// from W4 + 1 aligned words per row); rstride = bytes between the rows.
+template <int R, int W4>
+__device__ __forceinline__ void ref_rows(const uint32_t* s, int o, int rstride,
+                                         uint32_t (&out)[R][W4]) {
+    const int sh = (o & 3) << 3;
+    const uint32_t* b = s + (o >> 2);
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        uint32_t wv[W4 + 1];
+#pragma unroll
+        for (int w = 0; w <= W4; w++) wv[w] = b[r * (rstride >> 2) + w];
+#pragma unroll
+        for (int w = 0; w < W4; w++) out[r][w] = __funnelshift_r(wv[w], wv[w + 1], sh);
     }
 }
 
@@ -105,334 +160,291 @@ __device__ __forceinline__ int hcsp_dx(int k) {
 }
 __device__ __forceinline__ int hcsp_dy(int k) { return k < 5 ? 0 : (k == 5 ? -1 : 1); }
 
-// Warp-level bitmap test-and-set of the candidate handled by this lane.  Returns true when the
-// candidate is feasible (|q| <= p) and was not visited before.
-__device__ __forceinline__ bool visit(uint32_t* bm, int qx, int qy, int p, bool active) {
-    if (!active || qx < -p || qx > p || qy < -p || qy > p) return false;
-    const int side = 2 * p + 1;
-    const int idx = (qy + p) * side + (qx + p);
-    const uint32_t bit = 1u << (idx & 31);
-    const uint32_t old = atomicOr(&bm[idx >> 5], bit);
-    return (old & bit) == 0;
-}
-
 // ----------------------------------------------------------------------------------------
-// Per-block SAD engines.
-//   B = 16: lane = (r = lane>>2, w = lane&3) covers rows r and r+8, bytes 4w..4w+3: one
-//           candidate per warp pass, sum by REDUX.SUM.  Conflict-free LDS when the region
-//           pitch is 16*odd bytes.
-//   B = 8:  lane = (slot = lane>>3, r = lane&7) covers row r, 8 bytes, of candidate `slot`:
-//           four candidates per warp pass; slot sums (<= 16320) are packed two per 32-bit
-//           word so two REDUX.SUM give all four.
+// Lane-group state machine.
+//
+// Each pass evaluates the (up to) 4 candidate slots of one search pattern, given by a
+// pattern id:  0 S1A  HCSP points (0,0) (-1,0) (1,0) (-2,0)       [Step 1, first half]
+//              1 S1B  HCSP points (2,0) (0,-1) (0,1)               [Step 1, second half]
+//              2 S3H  HDSP (-2,0) (2,0) (0,-1) (0,1)               [Steps 2-3, P:257]
+//              3 S3V  VDSP (-1,0) (1,0) (0,-2) (0,2)
+//              4 S4H  middle points (-1,0) (1,0)                    [Step 4]
+//              5 S4V  middle points (0,-1) (0,1)
+//              6 PREH distant points (-2,0) (2,0)   (DCDS^S look-up, not counted)
+//              7 PREV distant points (0,-2) (0,2)
+// Slot order is the fixed pattern order of reading C7.  A table in shared memory holds, per
+// pattern, the byte offset of every slot in the staged region (dy*pitch + dx) and a packed
+// code word: bits 6k..6k+5 = (dx+2) | (dy+2) << 3 of slot k, bits 24..27 = slots in use.
 // ----------------------------------------------------------------------------------------
-template <int B>
-struct Engine;
+enum : int { ST_DONE = 0, ST_S1A = 1, ST_S1B = 2, ST_S3 = 3, ST_S4 = 4, ST_S4PRE = 5, ST_IDLE = 6 };
 
-template <>
-struct Engine<16> {
-    uint32_t c0, c1;  // current-block words held in registers
-    int lb0, lb1;     // lane byte offsets inside the candidate window
-
-    __device__ __forceinline__ void load(const uint8_t* scur, int TW, int lbx, int lby,
-                                         int pitch, int lane) {
-        const int r = lane >> 2, w = lane & 3;
-        const uint8_t* base = scur + (lby * 16 + r) * TW + lbx * 16 + 4 * w;
-        c0 = *reinterpret_cast<const uint32_t*>(base);
-        c1 = *reinterpret_cast<const uint32_t*>(base + 8 * TW);
-        lb0 = r * pitch + 4 * w;
-        lb1 = lb0 + 8 * pitch;
-    }
-    // SAD of one candidate at byte offset o (block origin + dy*pitch + dx) -- warp-uniform.
-    __device__ __forceinline__ uint32_t sad(const uint32_t* s, int o) const {
-        const uint32_t r0 = lds_u8x4(s, o + lb0);
-        const uint32_t r1 = lds_u8x4(s, o + lb1);
-        return __reduce_add_sync(FULL, vsad4(c1, r1, vsad4(c0, r0, 0u)));
-    }
-    __device__ __forceinline__ uint32_t sse(const uint32_t* s, int o) const {
-        const uint32_t r0 = lds_u8x4(s, o + lb0);
-        const uint32_t r1 = lds_u8x4(s, o + lb1);
-        return __reduce_add_sync(FULL, ssd4(c1, r1, ssd4(c0, r0, 0u)));
-    }
+// Pattern table (dx, dy per slot) -- the code words are built once per launch.
+struct PatTable {
+    int d[8][4][2];
+    uint32_t used[8];
 };
+constexpr PatTable kPat = {
+    {{{0, 0}, {-1, 0}, {1, 0}, {-2, 0}}, {{2, 0}, {0, -1}, {0, 1}, {0, 0}},
+     {{-2, 0}, {2, 0}, {0, -1}, {0, 1}}, {{-1, 0}, {1, 0}, {0, -2}, {0, 2}},
+     {{-1, 0}, {1, 0}, {0, 0}, {0, 0}},  {{0, -1}, {0, 1}, {0, 0}, {0, 0}},
+     {{-2, 0}, {2, 0}, {0, 0}, {0, 0}},  {{0, -2}, {0, 2}, {0, 0}, {0, 0}}},
+    {0xf, 0x7, 0xf, 0xf, 0x3, 0x3, 0x3, 0x3}};
 
-template <>
-struct Engine<8> {
-    uint32_t c0, c1;
-    int lb;
-    int slot;
-
-    __device__ __forceinline__ void load(const uint8_t* scur, int TW, int lbx, int lby,
-                                         int pitch, int lane) {
-        const int r = lane & 7;
-        slot = lane >> 3;
-        const uint8_t* base = scur + (lby * 8 + r) * TW + lbx * 8;
-        c0 = *reinterpret_cast<const uint32_t*>(base);
-        c1 = *reinterpret_cast<const uint32_t*>(base + 4);
-        lb = r * pitch;
-    }
-    // Four candidates: this lane evaluates the one of its slot at byte offset o.
-    // Returns packed sums: lo = {slot0 | slot1 << 16}, hi = {slot2 | slot3 << 16}.
-    __device__ __forceinline__ void sad4(const uint32_t* s, int o, uint32_t& s01,
-                                         uint32_t& s23) const {
-        const int a = o + lb;
-        const uint32_t w0 = s[a >> 2], w1 = s[(a >> 2) + 1], w2 = s[(a >> 2) + 2];
-        const int sh = (a & 3) << 3;
-        const uint32_t r0 = __funnelshift_r(w0, w1, sh), r1 = __funnelshift_r(w1, w2, sh);
-        uint32_t v = vsad4(c1, r1, vsad4(c0, r0, 0u));
-        v <<= (slot & 1) << 4;
-        s01 = __reduce_add_sync(FULL, slot < 2 ? v : 0u);
-        s23 = __reduce_add_sync(FULL, slot < 2 ? 0u : v);
-    }
-    // SSE at byte offset o using slot-0 lanes only.
-    __device__ __forceinline__ uint32_t sse(const uint32_t* s, int o) const {
-        const int a = o + lb;
-        const uint32_t w0 = s[a >> 2], w1 = s[(a >> 2) + 1], w2 = s[(a >> 2) + 2];
-        const int sh = (a & 3) << 3;
-        const uint32_t r0 = __funnelshift_r(w0, w1, sh), r1 = __funnelshift_r(w1, w2, sh);
-        const uint32_t v = ssd4(c1, r1, ssd4(c0, r0, 0u));
-        return __reduce_add_sync(FULL, slot == 0 ? v : 0u);
-    }
-};
-
-__device__ __forceinline__ uint32_t unpack4(uint32_t s01, uint32_t s23, int k) {
-    const uint32_t w = (k < 2) ? s01 : s23;
-    return (k & 1) ? (w >> 16) : (w & 0xffffu);
+inline constexpr uint32_t pat_code(int pid) {  // host side (kernel args)
+    uint32_t w = kPat.used[pid] << 24;
+    for (int k = 0; k < 4; k++)
+        w |= (uint32_t)((kPat.d[pid][k][0] + 2) | ((kPat.d[pid][k][1] + 2) << 3)) << (6 * k);
+    return w;
 }
+__device__ __forceinline__ int code_dx(uint32_t w, int k) { return (int)((w >> (6 * k)) & 7u) - 2; }
+__device__ __forceinline__ int code_dy(uint32_t w, int k) { return (int)((w >> (6 * k + 3)) & 7u) - 2; }
 
-// SAD of a single candidate at byte offset o (warp-uniform) for either engine.
-template <int B>
-__device__ __forceinline__ uint32_t sad1(const Engine<B>& E, const uint32_t* s, int o) {
-    if constexpr (B == 8) {
-        uint32_t a01, a23;
-        E.sad4(s, o, a01, a23);
-        return a01 & 0xffffu;
-    } else {
-        return E.sad(s, o);
-    }
-}
-
-// ----------------------------------------------------------------------------------------
-// The search of one block by one warp.  Returns (mx, my, sad, points); all warp-uniform.
-// VARIANT 0 = DCDS, 1 = DCDS^S.
-// ----------------------------------------------------------------------------------------
-template <int B, int VARIANT>
-__device__ __forceinline__ void dcds_block(const Engine<B>& E, const uint32_t* s, int base,
-                                           int pitch, int p, uint32_t* bm, int bm_words,
-                                           int lane, int& mx, int& my, uint32_t& best,
-                                           int& points) {
-    // fresh visited set (reading C5)
-    for (int i = lane * 4; i < bm_words; i += 128)
-        *reinterpret_cast<uint4*>(bm + i) = make_uint4(0, 0, 0, 0);
-    __syncwarp();
-
-    // ---- Step 1: HCSP at the origin, 7 points, k = 0 is the centre.
-    const int k1 = lane & 7;
-    const bool f1 = visit(bm, hcsp_dx(k1), hcsp_dy(k1), p, lane < 7);
-    const uint32_t m1 = __ballot_sync(FULL, f1) & 0x7f;
-    points = __popc(m1);
-    uint32_t s0;
-    uint32_t key = 0xffffffffu;  // (sad << 3) | k of the best new point
-    if constexpr (B == 8) {
-        // pass A: slots = HCSP k 0..3; pass B: k 4..6 (slot 3 idle -> centre)
-        const int slot = lane >> 3;
-        {
-            const int o = base + hcsp_dy(slot) * pitch + hcsp_dx(slot);
-            uint32_t a01, a23;
-            E.sad4(s, ((m1 >> slot) & 1) ? o : base, a01, a23);
-            s0 = unpack4(a01, a23, 0);
-#pragma unroll
-            for (int k = 1; k < 4; k++)
-                if ((m1 >> k) & 1) key = min(key, (unpack4(a01, a23, k) << 3) | k);
-        }
-        {
-            const int k = 4 + slot;
-            const bool ok = slot < 3 && ((m1 >> k) & 1);
-            const int o = base + hcsp_dy(k) * pitch + hcsp_dx(k);
-            uint32_t a01, a23;
-            E.sad4(s, ok ? o : base, a01, a23);
-#pragma unroll
-            for (int j = 0; j < 3; j++)
-                if ((m1 >> (4 + j)) & 1) key = min(key, (unpack4(a01, a23, j) << 3) | (4 + j));
-        }
-    } else {
-        s0 = E.sad(s, base);
-#pragma unroll
-        for (int k = 1; k < 7; k++)
-            if ((m1 >> k) & 1) key = min(key, (E.sad(s, base + hcsp_dy(k) * pitch + hcsp_dx(k)) << 3) | k);
-    }
-    best = s0;
-    int cx = 0, cy = 0;
-    if ((key >> 3) >= s0) {  // halfway stop
-        mx = 0; my = 0;
-        return;
-    }
-    best = key >> 3;
-    cx = hcsp_dx(key & 7);
-    cy = hcsp_dy(key & 7);
-    int kind = (cy == 0) ? 0 : 1;  // switching strategy one: 0 = HDSP, 1 = VDSP
-
-    // ---- Steps 2 and 3
-    uint32_t last_s01 = 0, last_s23 = 0;   // DCDS^S: SADs of the final pattern
-    uint32_t last_m = 0;
-    for (;;) {
-        const int kk = lane & 3;
-        const bool fk = visit(bm, cx + ddsp_dx(kind, kk), cy + ddsp_dy(kind, kk), p, lane < 4);
-        const uint32_t m = __ballot_sync(FULL, fk) & 0xf;
-        points += __popc(m);
-        key = 0xffffffffu;
-        const int cbase = base + cy * pitch + cx;
-        if constexpr (B == 8) {
-            const int slot = lane >> 3;
-            const int o = cbase + ddsp_dy(kind, slot) * pitch + ddsp_dx(kind, slot);
-            uint32_t a01, a23;
-            E.sad4(s, ((m >> slot) & 1) ? o : cbase, a01, a23);
-#pragma unroll
-            for (int k = 0; k < 4; k++)
-                if ((m >> k) & 1) key = min(key, (unpack4(a01, a23, k) << 2) | k);
-            last_s01 = a01; last_s23 = a23;
-        } else {
-            uint32_t mm = m;
-            last_s01 = 0; last_s23 = 0;
-            while (mm) {
-                const int k = __ffs(mm) - 1;
-                mm &= mm - 1;
-                const uint32_t v = E.sad(s, cbase + ddsp_dy(kind, k) * pitch + ddsp_dx(kind, k));
-                key = min(key, (v << 2) | k);
-                if (k < 2) last_s01 |= v << ((k & 1) << 4);
-                else last_s23 |= v << ((k & 1) << 4);
-            }
-        }
-        last_m = m;
-        if ((key >> 2) >= best) break;  // BMP at the centre -> Step 4
-        const int k = key & 3;
-        best = key >> 2;
-        cx += ddsp_dx(kind, k);
-        cy += ddsp_dy(kind, k);
-        if (ddsp_near(kind, k)) kind ^= 1;  // switching strategy two
-    }
-
-    // ---- Step 4: middle points of the final pattern, (-1,0),(1,0) or (0,-1),(0,1).
-    const int mdx0 = kind == 0 ? -1 : 0, mdy0 = kind == 0 ? 0 : -1;
-    bool want0 = true, want1 = true;
-    if constexpr (VARIANT == 1) {
-        // DCDS^S: only the side of the cheaper distant point (reading C22).
-        // Distant points of the final pattern: HDSP k = 0,1; VDSP k = 2,3.
-        const int kd = kind == 0 ? 0 : 2;
-        uint32_t dn = 0xffffffffu, dp = 0xffffffffu;
-        const int ax = kind == 0 ? 2 : 0, ay = kind == 0 ? 0 : 2;
-        const int cbase = base + cy * pitch + cx;
-        const bool fn = (cx - ax >= -p) && (cy - ay >= -p);
-        const bool fp = (cx + ax <= p) && (cy + ay <= p);
-        // a distant point scored in the final pass has its SAD at hand; one visited earlier
-        // is re-evaluated (same value as when it was scored; not counted again).
-        if (fn) {
-            dn = ((last_m >> kd) & 1) ? unpack4(last_s01, last_s23, kd) : 0xffffffffu;
-            if (dn == 0xffffffffu) dn = sad1<B>(E, s, cbase - ay * pitch - ax);
-        }
-        if (fp) {
-            dp = ((last_m >> (kd + 1)) & 1) ? unpack4(last_s01, last_s23, kd + 1) : 0xffffffffu;
-            if (dp == 0xffffffffu) dp = sad1<B>(E, s, cbase + ay * pitch + ax);
-        }
-        // infeasible distant point = +inf; choose the positive side only if strictly cheaper
-        const bool pos = (fp ? dp : 0xffffffffu) < (fn ? dn : 0xffffffffu) ||
-                         (fp && !fn);
-        want0 = !pos;
-        want1 = pos;
-    }
-    const int kk = lane & 1;
-    const bool fm = visit(bm, cx + (kk ? -mdx0 : mdx0), cy + (kk ? -mdy0 : mdy0), p,
-                          lane < 2 && (kk ? want1 : want0));
-    const uint32_t m4 = __ballot_sync(FULL, fm) & 0x3;
-    points += __popc(m4);
-    if (m4) {
-        const int cbase = base + cy * pitch + cx;
-        key = 0xffffffffu;
-        if constexpr (B == 8) {
-            const int slot = lane >> 3;
-            const int sg = (slot & 1) ? 1 : -1;
-            const int o = cbase + sg * (mdy0 * -1) * pitch + sg * (mdx0 * -1);
-            uint32_t a01, a23;
-            E.sad4(s, (slot < 2 && ((m4 >> slot) & 1)) ? o : cbase, a01, a23);
-#pragma unroll
-            for (int k = 0; k < 2; k++)
-                if ((m4 >> k) & 1) key = min(key, (unpack4(a01, a23, k) << 1) | k);
-        } else {
-            uint32_t mm = m4;
-            while (mm) {
-                const int k = __ffs(mm) - 1;
-                mm &= mm - 1;
-                const int sg = k ? 1 : -1;
-                key = min(key, (E.sad(s, cbase + sg * (-mdy0) * pitch + sg * (-mdx0)) << 1) | k);
-            }
-        }
-        if ((key >> 1) < best) {
-            const int k = key & 1;
-            const int sg = k ? 1 : -1;
-            best = key >> 1;
-            cx += sg * (-mdx0);
-            cy += sg * (-mdy0);
-        }
-    }
-    mx = cx;
-    my = cy;
-}
-
-template <int B, int NWARP, int VARIANT>
-__global__ void __launch_bounds__(NWARP * 32) dcds_kernel(const SearchArgs a) {
-    extern __shared__ __align__(16) uint8_t smem[];
+template <int B, int G, int NWARP, int VARIANT>
+__global__ void __launch_bounds__(NWARP * 32)
+    dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
+                const SearchArgs a) {
+    static_assert(G == 4 || G == 8 || G == 16, "lane-group size");
+    constexpr int R = B / G;      // rows per lane (lane j of a group: rows j, j+G, ...)
+    constexpr int W4 = B / 4;     // 32-bit words per block row
+    constexpr int NG = 32 / G;    // groups per warp
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ int4 s_poff[8];
+    __shared__ uint32_t s_pcode[8];
+    __shared__ __align__(8) uint64_t s_bar;
+    uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane % G, g = lane / G, leader = g * G;
     const int pair = blockIdx.y;
     const int tx = blockIdx.x % a.ntx, ty = blockIdx.x / a.ntx;
     const int TW = a.tbx * B, TH = a.tby * B;
     const int x0 = tx * TW, y0 = ty * TH;
     const int xs = (x0 - a.p) & ~15;  // floor to 16 (two's complement)
     const int ys = y0 - a.p;
-    const uint8_t* cur = a.cur0 + (long long)pair * a.stride;
-    const uint8_t* ref = a.ref0 + (long long)pair * a.stride;
+    const int pitch = a.pitch, p = a.p;
 
+    // shared layout: reference region (pitch x rh) | current tile (TW x TH) | bitmaps | stats
     uint8_t* sref = smem;
-    uint8_t* scur = smem + a.pitch * a.rh + 16;
+    uint8_t* scur = smem + a.cur_off;
     uint32_t* bms = reinterpret_cast<uint32_t*>(scur + TW * TH);
-    uint32_t* bm = bms + warp * a.bm_words;
-    unsigned long long* cst = reinterpret_cast<unsigned long long*>(bms + NWARP * a.bm_words);
+    uint32_t* bm = bms + (warp * NG + g) * a.bm_words;
+    unsigned long long* cst = reinterpret_cast<unsigned long long*>(bms + NWARP * NG * a.bm_words);
     int* ctr = reinterpret_cast<int*>(cst + 3);
 
+    // ---- stage the tile with TMA: reference region + current tile, one mbarrier
+    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&s_bar, (uint32_t)(pitch * a.rh + TW * TH));
+        tma_load_3d(sref, &tm_ref, xs, ys, pair, &s_bar);
+        tma_load_3d(scur, &tm_cur, x0, y0, pair, &s_bar);
+    }
     if (threadIdx.x < 3) cst[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) *ctr = 0;
-    stage_tile(a, cur, ref, xs, ys, x0, y0, TW, TH, sref, scur);
+    if (threadIdx.x < 8) {
+        const uint32_t w = a.pcode[threadIdx.x];
+        s_pcode[threadIdx.x] = w;
+        s_poff[threadIdx.x] = make_int4(code_dy(w, 0) * pitch + code_dx(w, 0),
+                                        code_dy(w, 1) * pitch + code_dx(w, 1),
+                                        code_dy(w, 2) * pitch + code_dx(w, 2),
+                                        code_dy(w, 3) * pitch + code_dx(w, 3));
+    }
+    mbar_wait(&s_bar, 0);
+    if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
+        fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
     __syncthreads();
 
     const uint32_t* s = reinterpret_cast<const uint32_t*>(sref);
-    const int nbt = a.tbx * a.tby;
+    const int rstride = G * pitch;  // bytes between a lane's rows
+    const int jrow = j * pitch;     // byte offset of the lane's first row
+    const int nby = a.nb / a.nbx;
+    const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, nby - ty * a.tby);
+    const int nbt = tbx_e * tby_e;
+    const float inv_tbx = 1.0f / (float)tbx_e;
+
+    // group state (every lane of a group holds the same values)
+    int st = ST_DONE, pid = 0, kind = 0, cx = 0, cy = 0, pts = 0, want = 3;
+    int bofs = 0, cpos = 0;
+    long long gblk = 0;
+    uint32_t best = 0, s0 = 0, key1 = 0xffffffffu;
+    uint32_t cw[R][W4];
+#pragma unroll
+    for (int r = 0; r < R; r++)
+#pragma unroll
+        for (int w = 0; w < W4; w++) cw[r][w] = 0;
     unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
+
     for (;;) {
-        int i = 0;
-        if (lane == 0) i = atomicAdd(ctr, 1);
-        i = __shfl_sync(FULL, i, 0);
-        if (i >= nbt) break;
-        const int lbx = i % a.tbx, lby = i / a.tbx;
-        const int bxg = x0 + lbx * B, byg = y0 + lby * B;
-        if (bxg >= a.W || byg >= a.H) continue;
-        Engine<B> E;
-        E.load(scur, TW, lbx, lby, a.pitch, lane);
-        const int base = (byg - ys) * a.pitch + (bxg - xs);
-        int mx, my, points;
-        uint32_t best;
-        dcds_block<B, VARIANT>(E, s, base, a.pitch, a.p, bm, a.bm_words, lane, mx, my, best,
-                               points);
-        const uint32_t sse = E.sse(s, base + my * a.pitch + mx);
-        if (lane == 0) {
-            const long long g = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
-            a.mv[g] = (uint32_t)(mx & 0xffff) | ((uint32_t)my << 16);
-            a.sad[g] = best;
-            a.pts[g] = (uint16_t)points;
-            acc_pts += (unsigned)points;
-            acc_sad += best;
-            acc_sse += sse;
+        // ---- groups that are done take the next block of the tile
+        const bool need = (st == ST_DONE);
+        const unsigned ball = __ballot_sync(FULL, need && j == 0);
+        if (ball) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(ctr, __popc(ball));
+            base = __shfl_sync(FULL, base, 0);
+            int idx = base + __popc(ball & ((1u << lane) - 1u));
+            idx = __shfl_sync(FULL, idx, leader);
+            if (need) {
+                if (idx < nbt) {
+                    // idx / tbx_e in float is exact here: idx < 2^16, tbx_e <= 2^8
+                    const int lby = (int)(((float)idx + 0.5f) * inv_tbx);
+                    const int lbx = idx - lby * tbx_e;
+                    const int bxg = x0 + lbx * B, byg = y0 + lby * B;
+                    bofs = (byg - ys) * pitch + (bxg - xs);
+                    cpos = bofs;
+                    gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
+#pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        const uint32_t* crow = reinterpret_cast<const uint32_t*>(
+                            scur + (lby * B + j + G * r) * TW + lbx * B);
+#pragma unroll
+                        for (int w = 0; w < W4; w++) cw[r][w] = crow[w];
+                    }
+                    for (int w = j * 4; w < a.bm_words; w += 4 * G)
+                        *reinterpret_cast<uint4*>(bm + w) = make_uint4(0, 0, 0, 0);
+                    st = ST_S1A; pid = 0; kind = 0; cx = 0; cy = 0; pts = 0; want = 3;
+                    key1 = 0xffffffffu;
+                } else {
+                    st = ST_IDLE;
+                }
+            }
+            __syncwarp();
+        }
+        if (__all_sync(FULL, st == ST_IDLE)) break;
+
+        const uint32_t pw = s_pcode[pid];
+        const int4 po = s_poff[pid];
+        const uint32_t used = (st == ST_IDLE) ? 0u : ((pw >> 24) & (st == ST_S4 ? (uint32_t)want : 0xfu));
+
+        // ---- visited-set test-and-set: lane j < 4 of each group owns slot j (reading C5)
+        bool nw = false;
+        if (j < 4 && ((used >> j) & 1)) {
+            const int qx = cx + code_dx(pw, j), qy = cy + code_dy(pw, j);
+            if (qx >= -p && qx <= p && qy >= -p && qy <= p) {  // window only (reading C8)
+                if (st == ST_S4PRE) {
+                    nw = true;  // DCDS^S look-up of the distant points: not scored again
+                } else {
+                    const int idx = (qy + p) * (2 * p + 1) + (qx + p);
+                    const uint32_t bit = 1u << (idx & 31);
+                    nw = (atomicOr(&bm[idx >> 5], bit) & bit) == 0;
+                }
+            }
+        }
+        const unsigned m4 = (__ballot_sync(FULL, nw) >> leader) & 0xfu;
+
+        // ---- SADs of the 4 slots over this lane's rows, packed and reduced over the group
+        const int ok[4] = {po.x, po.y, po.z, po.w};
+        uint32_t sadk[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            uint32_t acc = 0;
+            if ((m4 >> k) & 1) {  // slots not scored this pass issue no shared-memory loads
+                uint32_t rw[R][W4];
+                ref_rows<R, W4>(s, cpos + ok[k] + jrow, rstride, rw);
+#pragma unroll
+                for (int r = 0; r < R; r++)
+#pragma unroll
+                    for (int w = 0; w < W4; w++) acc = vsad4(cw[r][w], rw[r][w], acc);
+            }
+            sadk[k] = acc;
+        }
+        uint32_t v01 = sadk[0] | (sadk[1] << 16), v23 = sadk[2] | (sadk[3] << 16);
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+            v01 += __shfl_xor_sync(FULL, v01, o);
+            v23 += __shfl_xor_sync(FULL, v23, o);
+        }
+        sadk[0] = v01 & 0xffffu; sadk[1] = v01 >> 16;
+        sadk[2] = v23 & 0xffffu; sadk[3] = v23 >> 16;
+
+        // ---- argmin over the new points of this pass, (SAD, slot) keys (reading C6/C7)
+        uint32_t key = 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if ((m4 >> k) & 1) key = min(key, (sadk[k] << 2) | k);
+        const int kb = key & 3;
+        const int mdx = code_dx(pw, kb), mdy = code_dy(pw, kb);
+        const int mo = kb == 0 ? po.x : kb == 1 ? po.y : kb == 2 ? po.z : po.w;
+
+        // ---- advance the state machine (group-uniform)
+        bool fin = false;
+        if (st != ST_S4PRE) pts += __popc(m4);
+        if (st == ST_S1A) {
+            // Step 1, first half: the centre (slot 0) is the incumbent
+            s0 = sadk[0];
+            uint32_t kk = 0xffffffffu;
+#pragma unroll
+            for (int k = 1; k < 4; k++)
+                if ((m4 >> k) & 1) kk = min(kk, (sadk[k] << 3) | k);
+            key1 = kk;
+            st = ST_S1B; pid = 1;
+        } else if (st == ST_S1B) {
+            uint32_t kk = key1;
+            if (key != 0xffffffffu) kk = min(kk, ((key >> 2) << 3) | (4 + kb));
+            if ((kk >> 3) < s0) {
+                best = kk >> 3;
+                const int h = kk & 7;
+                cx = hcsp_dx(h);
+                cy = hcsp_dy(h);
+                cpos = bofs + cy * pitch + cx;
+                kind = (cy == 0) ? 0 : 1;  // switching strategy one
+                st = ST_S3; pid = 2 + kind;
+            } else {  // halfway stop
+                best = s0;
+                fin = true;
+            }
+        } else if (st == ST_S3) {
+            // Step 2 / Step 3
+            if ((key >> 2) < best) {
+                best = key >> 2;
+                cx += mdx; cy += mdy; cpos += mo;
+                if ((kb >= 2) != (kind == 1)) { kind ^= 1; pid ^= 1; }  // near point
+            } else {
+                st = VARIANT ? ST_S4PRE : ST_S4;  // BMP at the centre -> Step 4
+                pid = (VARIANT ? 6 : 4) + kind;
+                want = 3;
+            }
+        } else if (st == ST_S4PRE) {
+            // DCDS^S: keep only the middle point beside the cheaper distant point;
+            // an infeasible distant point costs +inf, ties go to the negative side (C22)
+            const uint32_t dn = (m4 & 1) ? sadk[0] : 0xffffffffu;
+            const uint32_t dp = (m4 & 2) ? sadk[1] : 0xffffffffu;
+            want = (dp < dn) ? 2 : 1;
+            st = ST_S4; pid = 4 + kind;
+        } else if (st == ST_S4) {
+            // Step 4: strict minimum of the middle points against the centre
+            if ((key >> 2) < best) {
+                best = key >> 2;
+                cx += mdx; cy += mdy; cpos += mo;
+            }
+            fin = true;
+        }
+
+        // ---- finished blocks: SSE of the compensated block (P:342 aspect 4), outputs
+        if (__any_sync(FULL, fin)) {
+            uint32_t ss = 0;
+            uint32_t rw[R][W4];
+            ref_rows<R, W4>(s, cpos + jrow, rstride, rw);
+#pragma unroll
+            for (int r = 0; r < R; r++)
+#pragma unroll
+                for (int w = 0; w < W4; w++) ss = ssd4(cw[r][w], rw[r][w], ss);
+#pragma unroll
+            for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
+            if (fin) {
+                if (j == 0) {
+                    a.mv[gblk] = (uint32_t)(cx & 0xffff) | ((uint32_t)cy << 16);
+                    a.sad[gblk] = best;
+                    a.pts[gblk] = (uint16_t)pts;
+                    acc_pts += (unsigned)pts;
+                    acc_sad += best;
+                    acc_sse += ss;
+                }
+                st = ST_DONE;
+            }
         }
     }
     if (a.stats) {
-        if (lane == 0) {
+        if (j == 0) {
             atomicAdd(&cst[0], acc_pts);
             atomicAdd(&cst[1], acc_sad);
             atomicAdd(&cst[2], acc_sse);

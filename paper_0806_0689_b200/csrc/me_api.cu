@@ -3,9 +3,12 @@
 // Every entry point validates its arguments before any device work and launches the
 // sm_100a kernels of dcds_kernel.cuh / fs_kernel.cuh on the library stream.  There is no
 // CPU fallback: without a working sm_100 device every call fails with ME_ENOTINIT/ME_ECUDA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -24,6 +27,7 @@ unsigned long long* g_scratch = nullptr;  // device u64 scratch (me_mc_psnr)
 char g_err[512] = "";
 long long g_launches = 0;
 int g_smem_optin = 0;
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;  // driver entry point (no -lcuda)
 
 // grow-only staging buffers of me_dcds_batch_host (two sets for double buffering)
 struct HostStage {
@@ -34,7 +38,7 @@ struct HostStage {
 };
 HostStage g_stage[2];
 
-constexpr int kNWarp = 8;
+constexpr int kNWarp = 4;
 
 int set_cuda_err(cudaError_t e, const char* where) {
     snprintf(g_err, sizeof g_err, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
@@ -87,14 +91,31 @@ struct DcdsLaunch {
     me::SearchArgs a;
     dim3 grid;
     size_t smem;
+    int G;
+    int TW, TH;
 };
 
+// Launch geometry: lane-group size G, tile of tbx x tby blocks.
+// ME_G / ME_TILE=tbx,tby override the defaults (tuning only).
 DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     DcdsLaunch L;
     me::SearchArgs& a = L.a;
     const int nbx = W / B, nby = H / B;
+    L.G = (B == 16) ? 8 : 4;
+
     int tbx = (B == 16) ? 8 : 16;
-    int tby = (B == 16) ? (p <= 8 ? 2 : 4) : (p <= 8 ? 4 : 8);
+    int tby = (B == 16) ? 2 : 4;  // measured on B200 (profiles/r1/TUNING.md)
+    if (const char* e = getenv("ME_G")) {
+        const int g = atoi(e);
+        if (g == 4 || g == 8) L.G = g;
+    }
+    if (const char* e = getenv("ME_TILE")) {
+        int tx = 0, ty = 0;
+        if (sscanf(e, "%d,%d", &tx, &ty) == 2 && tx > 0 && ty > 0 && (tx * B) % 16 == 0) {
+            tbx = tx;
+            tby = ty;
+        }
+    }
     tbx = std::min(tbx, nbx);
     tby = std::min(tby, nby);
     const int TW = tbx * B, TH = tby * B;
@@ -104,7 +125,7 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     const int nty = (nby + tby - 1) / tby;
     // region width: x0 - xs <= p + 15, plus TW + p, plus 16 bytes of over-read slack
     int pitch = ((TW + 2 * p + 31) + 15) & ~15;
-    if (((pitch >> 4) & 1) == 0) pitch += 16;  // 16 * odd: conflict-free rows for the B=16 engine
+    if (((pitch >> 4) & 1) == 0) pitch += 16;  // 16 * odd bytes: rows spread over the banks
     a.pitch = pitch;
     a.rh = TH + 2 * p;
     const int side = 2 * p + 1;
@@ -112,13 +133,46 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     a.nbx = nbx;
     a.nb = nbx * nby;
     L.grid = dim3(a.ntx * nty, npairs);
-    L.smem = (size_t)pitch * a.rh + 16 + (size_t)TW * TH + (size_t)kNWarp * a.bm_words * 4 + 32;
+    for (int i = 0; i < 8; i++) a.pcode[i] = me::pat_code(i);
+    const int groups = kNWarp * 32 / L.G;
+    a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;  // TMA destinations are 128-byte aligned
+    L.TW = TW; L.TH = TH;
+    L.smem = 128 + (size_t)a.cur_off + (size_t)TW * TH + (size_t)groups * a.bm_words * 4 + 32;
     return L;
 }
 
+template <int B, int G, int VARIANT>
+void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap& tr, cudaStream_t s) {
+    me::dcds_kernel<B, G, kNWarp, VARIANT><<<L.grid, kNWarp * 32, L.smem, s>>>(tc, tr, L.a);
+}
+
 template <int B, int VARIANT>
-void launch_dcds_t(const DcdsLaunch& L, cudaStream_t s) {
-    me::dcds_kernel<B, kNWarp, VARIANT><<<L.grid, kNWarp * 32, L.smem, s>>>(L.a);
+void launch_dcds_b(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap& tr, cudaStream_t s) {
+    if (L.G == 8) launch_dcds_t<B, 8, VARIANT>(L, tc, tr, s);
+    else launch_dcds_t<B, 4, VARIANT>(L, tc, tr, s);
+}
+
+#define ME_DCDS_KERNELS(X) \
+    X(16, 8, 0) X(16, 8, 1) X(16, 4, 0) X(16, 4, 1) X(8, 8, 0) X(8, 8, 1) X(8, 4, 0) X(8, 4, 1)
+
+// 3-D tiled tensor map over npairs frames (x = column, y = row, z = pair) for TMA.
+int make_tmap(CUtensorMap* tm, const uint8_t* base, int W, int H, int npairs, long long stride,
+              int box_w, int box_h) {
+    if (!g_encode) return fail(ME_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    if (box_w > 256 || box_h > 256 || (box_w & 15)) return fail(ME_EINVAL, "TMA box too large");
+    cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)npairs};
+    cuuint64_t strides[2] = {(cuuint64_t)W, (cuuint64_t)(npairs > 1 ? stride : (long long)W * H)};
+    cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(base), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return ME_ECUDA;
+    }
+    return ME_OK;
 }
 
 int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W, int H,
@@ -131,11 +185,16 @@ int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npa
     L.a.sad = sad;
     L.a.pts = pts;
     L.a.stats = reinterpret_cast<unsigned long long*>(stats);
+    CUtensorMap tc, tr;
+    int rc = make_tmap(&tc, cur0, W, H, npairs, stride, L.TW, L.TH);
+    if (rc) return rc;
+    rc = make_tmap(&tr, ref0, W, H, npairs, stride, L.a.pitch, L.a.rh);
+    if (rc) return rc;
     if (stats) CK(cudaMemsetAsync(stats, 0, sizeof(uint64_t) * 3 * (size_t)npairs, s));
     if (block == 16) {
-        if (variant) launch_dcds_t<16, 1>(L, s); else launch_dcds_t<16, 0>(L, s);
+        if (variant) launch_dcds_b<16, 1>(L, tc, tr, s); else launch_dcds_b<16, 0>(L, tc, tr, s);
     } else {
-        if (variant) launch_dcds_t<8, 1>(L, s); else launch_dcds_t<8, 0>(L, s);
+        if (variant) launch_dcds_b<8, 1>(L, tc, tr, s); else launch_dcds_b<8, 0>(L, tc, tr, s);
     }
     g_launches++;
     CK(cudaGetLastError());
@@ -221,13 +280,19 @@ int me_init(int device) {
     }
     g_smem_optin = (int)prop.sharedMemPerBlockOptin;
     int rc;
-    if ((rc = allow_smem(me::dcds_kernel<16, kNWarp, 0>))) return rc;
-    if ((rc = allow_smem(me::dcds_kernel<16, kNWarp, 1>))) return rc;
-    if ((rc = allow_smem(me::dcds_kernel<8, kNWarp, 0>))) return rc;
-    if ((rc = allow_smem(me::dcds_kernel<8, kNWarp, 1>))) return rc;
+#define ME_ALLOW(B, G, V) \
+    if ((rc = allow_smem(me::dcds_kernel<B, G, kNWarp, V>))) return rc;
+    ME_DCDS_KERNELS(ME_ALLOW)
+#undef ME_ALLOW
     if ((rc = allow_smem(me::fs_kernel<16>))) return rc;
     if ((rc = allow_smem(me::fs_kernel<8>))) return rc;
     if (!g_scratch) CK(cudaMalloc(&g_scratch, 64));
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_encode),
+                                   cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess) return fail(ME_ECUDA, "cuTensorMapEncodeTiled not found");
+    }
     for (auto& cs : g_copy_streams)
         if (!cs) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     g_dev = device;
