@@ -214,6 +214,8 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_0806_0689_b200 as me
@@ -231,20 +233,17 @@ def main():
     torch.cuda.synchronize()
 
     if ws > 1:
-        import torch.distributed as dist
-        # one packed record per block: mv (4 B) + sad (4 B) + points (2 B), plus per-pair stats
-        g_mv = torch.empty(ws * n * cfg.nb * 2, dtype=torch.int16, device=dev)
-        g_sad = torch.empty(ws * n * cfg.nb, dtype=torch.int32, device=dev)
-        g_pts = torch.empty(ws * n * cfg.nb, dtype=torch.int16, device=dev)
-        g_st = torch.empty(ws * n * 3, dtype=torch.int64, device=dev)
+        from paper_0806_0689_b200 import dist as mdist
+
+    def gather():
+        # NCCL all_gather of every rank's per-pair MV field + statistics (one packed record
+        # per pair; paper_0806_0689_b200/dist.py) -- the path's only collective
+        if ws > 1:
+            mdist.gather_fields(mv, sad, pts, st, ws * n)
 
     def step():
         me.me_dcds_batch(frames, cfg.B, cfg.p, mv, sad, pts, st)
-        if ws > 1:
-            dist.all_gather_into_tensor(g_mv, mv.view(-1))
-            dist.all_gather_into_tensor(g_sad, sad.view(-1))
-            dist.all_gather_into_tensor(g_pts, pts.view(-1))
-            dist.all_gather_into_tensor(g_st, st.view(-1))
+        gather()
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -263,11 +262,7 @@ def main():
             ev[k][0].record(stream)
             me.me_dcds_batch(frames, cfg.B, cfg.p, mv, sad, pts, st)
             ev[k][1].record(stream)
-            if ws > 1:
-                dist.all_gather_into_tensor(g_mv, mv.view(-1))
-                dist.all_gather_into_tensor(g_sad, sad.view(-1))
-                dist.all_gather_into_tensor(g_pts, pts.view(-1))
-                dist.all_gather_into_tensor(g_st, st.view(-1))
+            gather()
         t_end.record(stream)
         torch.cuda.synchronize()
     launches = me.me_launch_count() - launches0

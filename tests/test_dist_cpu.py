@@ -1,0 +1,98 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): pair sharding, packed all_gather of the
+per-pair MV fields + statistics, reassembly.  The per-rank search is the oracle here (no GPU);
+on B200 ranks run libme.so and gather with NCCL through the same code (bench.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_0806_0689_b200 import dist as mdist
+from paper_0806_0689_b200 import synth
+
+
+def test_shard_ranges():
+    for n, w in [(239, 8), (959, 8), (29, 2), (1, 4), (7, 2), (16, 4)]:
+        ranges = [mdist.shard(n, w, r) for r in range(w)]
+        assert ranges[0][0] == 0 and ranges[-1][1] == n
+        for (a, b), (c, d) in zip(ranges, ranges[1:]):
+            assert b == c and a <= b
+        assert max(b - a for a, b in ranges) == mdist.shard_size(n, w)
+
+
+def test_pack_roundtrip():
+    g = torch.Generator().manual_seed(0)
+    for nb in (99, 396, 7):
+        n = 3
+        mv = torch.randint(-32, 33, (n, nb, 2), generator=g, dtype=torch.int16)
+        sad = torch.randint(0, 65281, (n, nb), generator=g, dtype=torch.int32)
+        pts = torch.randint(1, 4226, (n, nb), generator=g, dtype=torch.int16)
+        st = torch.randint(0, 2**40, (n, 3), generator=g, dtype=torch.int64)
+        rec = mdist.pack_fields(mv, sad, pts, st, 5)
+        assert rec.shape[0] == 5
+        m2, s2, p2, t2 = mdist.unpack_fields(rec[:n], nb)
+        assert torch.equal(m2, mv) and torch.equal(s2, sad) and torch.equal(p2, pts) and torch.equal(t2, st)
+
+
+def _oracle_fields(frames, B, p):
+    mvs, sads, ptss, sts = [], [], [], []
+    for t in range(frames.shape[0]):
+        mv, sad, pts = oracle.dcds(frames[t, 0], frames[t, 1], B, p)
+        _, sse = oracle.mc_psnr(frames[t, 0], frames[t, 1], B, mv)
+        mvs.append(mv)
+        sads.append(sad.astype(np.int32))
+        ptss.append(pts.astype(np.int16))
+        sts.append([int(pts.astype(np.int64).sum()), int(sad.astype(np.int64).sum()), sse])
+    return (torch.from_numpy(np.stack(mvs)), torch.from_numpy(np.stack(sads)),
+            torch.from_numpy(np.stack(ptss)), torch.tensor(sts, dtype=torch.int64))
+
+
+def _worker(rank, world, port, frames, B, p, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = frames.shape[0]
+    lo, hi = mdist.shard(n, world, rank)
+    mv, sad, pts, st = _oracle_fields(frames[lo:hi], B, p)
+    if hi == lo:
+        nb = (frames.shape[3] // B) * (frames.shape[2] // B)
+        mv = torch.zeros(0, nb, 2, dtype=torch.int16)
+        sad = torch.zeros(0, nb, dtype=torch.int32)
+        pts = torch.zeros(0, nb, dtype=torch.int16)
+        st = torch.zeros(0, 3, dtype=torch.int64)
+    g = mdist.gather_fields(mv, sad, pts, st, n)
+    if rank == 0:
+        out_q.put([t.numpy() for t in g])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("world,npairs", [(2, 7), (2, 2)])
+def test_gloo_gather_matches_single_rank(world, npairs):
+    cfg = synth.CONFIGS["c1"]
+    frames = synth.make_sequence(cfg, pairs=range(1, npairs + 1)).numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, frames, cfg.B, cfg.p, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    ref = [t.numpy() for t in _oracle_fields(frames, cfg.B, cfg.p)]
+    for a, b in zip(got, ref):
+        np.testing.assert_array_equal(a, b)

@@ -275,3 +275,29 @@ def test_errors_raise():
     out = me.alloc_outputs(1, 20, DEV)
     with pytest.raises(me.MEError):
         me.me_dcds_batch(fr, 16, 7, *out)     # 40 % 16 != 0
+
+
+def test_nccl_gather_single_rank():
+    """The NCCL gather path of bench.py (world size 1 on one GPU: the collective runs, and the
+    gathered fields equal the local ones byte for byte)."""
+    import socket
+    import torch.distributed as dist
+    from paper_0806_0689_b200 import dist as mdist
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=DEV)
+    try:
+        cfg = synth.CONFIGS["c1"]
+        fr = synth.make_sequence(cfg, device=DEV, pairs=range(1, 6))
+        out = me.alloc_outputs(5, cfg.nb, DEV)
+        me.me_dcds_batch(fr, cfg.B, cfg.p, *out)
+        g = mdist.gather_fields(*out, 5)
+        for a, b in zip(g, out):
+            assert torch.equal(a, b)
+    finally:
+        dist.destroy_process_group()
