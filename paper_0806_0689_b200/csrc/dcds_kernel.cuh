@@ -227,8 +227,7 @@ __global__ void __launch_bounds__(NWARP * 32)
     uint8_t* scur = smem + a.cur_off;
     uint32_t* bms = reinterpret_cast<uint32_t*>(scur + TW * TH);
     uint32_t* bm = bms + (warp * NG + g) * a.bm_words;
-    unsigned long long* cst = reinterpret_cast<unsigned long long*>(bms + NWARP * NG * a.bm_words);
-    int* ctr = reinterpret_cast<int*>(cst + 3);
+    int* ctr = reinterpret_cast<int*>(bms + NWARP * NG * a.bm_words);
 
     // ---- stage the tile with TMA: reference region + current tile, one mbarrier
     if (threadIdx.x == 0) mbar_init(&s_bar, 1);
@@ -238,7 +237,6 @@ __global__ void __launch_bounds__(NWARP * 32)
         tma_load_3d(sref, &tm_ref, xs, ys, pair, &s_bar);
         tma_load_3d(scur, &tm_cur, x0, y0, pair, &s_bar);
     }
-    if (threadIdx.x < 3) cst[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) *ctr = 0;
     if (threadIdx.x < 8) {
         const uint32_t w = a.pcode[threadIdx.x];
@@ -422,12 +420,14 @@ __global__ void __launch_bounds__(NWARP * 32)
         // ---- finished blocks: SSE of the compensated block (P:342 aspect 4), outputs
         if (__any_sync(FULL, fin)) {
             uint32_t ss = 0;
-            uint32_t rw[R][W4];
-            ref_rows<R, W4>(s, cpos + jrow, rstride, rw);
+            if (fin) {  // only finishing groups read shared memory
+                uint32_t rw[R][W4];
+                ref_rows<R, W4>(s, cpos + jrow, rstride, rw);
 #pragma unroll
-            for (int r = 0; r < R; r++)
+                for (int r = 0; r < R; r++)
 #pragma unroll
-                for (int w = 0; w < W4; w++) ss = ssd4(cw[r][w], rw[r][w], ss);
+                    for (int w = 0; w < W4; w++) ss = ssd4(cw[r][w], rw[r][w], ss);
+            }
 #pragma unroll
             for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
             if (fin) {
@@ -443,14 +443,18 @@ __global__ void __launch_bounds__(NWARP * 32)
             }
         }
     }
-    if (a.stats) {
-        if (j == 0) {
-            atomicAdd(&cst[0], acc_pts);
-            atomicAdd(&cst[1], acc_sad);
-            atomicAdd(&cst[2], acc_sse);
+    if (a.stats) {  // per-pair statistics: warp sums of the group leaders, 3 atomics per warp
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            acc_pts += __shfl_xor_sync(FULL, acc_pts, o);
+            acc_sad += __shfl_xor_sync(FULL, acc_sad, o);
+            acc_sse += __shfl_xor_sync(FULL, acc_sse, o);
         }
-        __syncthreads();
-        if (threadIdx.x < 3) atomicAdd(&a.stats[pair * 3 + threadIdx.x], cst[threadIdx.x]);
+        if (lane == 0) {
+            atomicAdd(&a.stats[pair * 3 + 0], acc_pts);
+            atomicAdd(&a.stats[pair * 3 + 1], acc_sad);
+            atomicAdd(&a.stats[pair * 3 + 2], acc_sse);
+        }
     }
 }
 
