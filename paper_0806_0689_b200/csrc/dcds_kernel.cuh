@@ -203,7 +203,7 @@ template <int B, int G, int NWARP, int VARIANT>
 __global__ void __launch_bounds__(NWARP * 32)
     dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
                 const SearchArgs a) {
-    static_assert(G == 4 || G == 8 || G == 16, "lane-group size");
+    static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "lane-group size");
     constexpr int R = B / G;      // rows per lane (lane j of a group: rows j, j+G, ...)
     constexpr int W4 = B / 4;     // 32-bit words per block row
     constexpr int NG = 32 / G;    // groups per warp
@@ -313,21 +313,27 @@ __global__ void __launch_bounds__(NWARP * 32)
         const int4 po = s_poff[pid];
         const uint32_t used = (st == ST_IDLE) ? 0u : ((pw >> 24) & (st == ST_S4 ? (uint32_t)want : 0xfu));
 
-        // ---- visited-set test-and-set: lane j < 4 of each group owns slot j (reading C5)
-        bool nw = false;
-        if (j < 4 && ((used >> j) & 1)) {
-            const int qx = cx + code_dx(pw, j), qy = cy + code_dy(pw, j);
-            if (qx >= -p && qx <= p && qy >= -p && qy <= p) {  // window only (reading C8)
-                if (st == ST_S4PRE) {
-                    nw = true;  // DCDS^S look-up of the distant points: not scored again
-                } else {
-                    const int idx = (qy + p) * (2 * p + 1) + (qx + p);
-                    const uint32_t bit = 1u << (idx & 31);
-                    nw = (atomicOr(&bm[idx >> 5], bit) & bit) == 0;
+        // ---- visited-set test-and-set (reading C5): lane j of a group owns slots j, j+G, ...
+        unsigned m4 = 0;
+#pragma unroll
+        for (int h = 0; h < (G >= 4 ? 1 : 4 / G); h++) {
+            const int k = j + h * G;
+            bool nw = false;
+            if (k < 4 && ((used >> k) & 1)) {
+                const int qx = cx + code_dx(pw, k), qy = cy + code_dy(pw, k);
+                if (qx >= -p && qx <= p && qy >= -p && qy <= p) {  // window only (reading C8)
+                    if (st == ST_S4PRE) {
+                        nw = true;  // DCDS^S look-up of the distant points: not scored again
+                    } else {
+                        const int idx = (qy + p) * (2 * p + 1) + (qx + p);
+                        const uint32_t bit = 1u << (idx & 31);
+                        nw = (atomicOr(&bm[idx >> 5], bit) & bit) == 0;
+                    }
                 }
             }
+            const unsigned bb = __ballot_sync(FULL, nw) >> leader;
+            m4 |= (G >= 4 ? (bb & 0xfu) : ((bb & ((1u << G) - 1u)) << (h * G)));
         }
-        const unsigned m4 = (__ballot_sync(FULL, nw) >> leader) & 0xfu;
 
         // ---- SADs of the 4 slots over this lane's rows, packed and reduced over the group
         const int ok[4] = {po.x, po.y, po.z, po.w};

@@ -101,13 +101,13 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     DcdsLaunch L;
     me::SearchArgs& a = L.a;
     const int nbx = W / B, nby = H / B;
-    L.G = (B == 16) ? 8 : 4;
+    L.G = (B == 16) ? 8 : 2;
 
     int tbx = (B == 16) ? 8 : 16;
     int tby = (B == 16) ? 2 : 4;  // measured on B200 (profiles/r1/TUNING.md)
     if (const char* e = getenv("ME_G")) {
         const int g = atoi(e);
-        if (g == 4 || g == 8) L.G = g;
+        if (g == 1 || g == 2 || g == 4 || g == 8) L.G = g;
     }
     if (const char* e = getenv("ME_TILE")) {
         int tx = 0, ty = 0;
@@ -149,11 +149,14 @@ void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap
 template <int B, int VARIANT>
 void launch_dcds_b(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap& tr, cudaStream_t s) {
     if (L.G == 8) launch_dcds_t<B, 8, VARIANT>(L, tc, tr, s);
+    else if (L.G == 2) launch_dcds_t<B, 2, VARIANT>(L, tc, tr, s);
+    else if (B == 8 && L.G == 1) launch_dcds_t<8, 1, VARIANT>(L, tc, tr, s);
     else launch_dcds_t<B, 4, VARIANT>(L, tc, tr, s);
 }
 
 #define ME_DCDS_KERNELS(X) \
-    X(16, 8, 0) X(16, 8, 1) X(16, 4, 0) X(16, 4, 1) X(8, 8, 0) X(8, 8, 1) X(8, 4, 0) X(8, 4, 1)
+    X(16, 8, 0) X(16, 8, 1) X(16, 4, 0) X(16, 4, 1) X(16, 2, 0) X(16, 2, 1) X(8, 8, 0) X(8, 8, 1) \
+    X(8, 4, 0) X(8, 4, 1) X(8, 2, 0) X(8, 2, 1) X(8, 1, 0) X(8, 1, 1)
 
 // 3-D tiled tensor map over npairs frames (x = column, y = row, z = pair) for TMA.
 int make_tmap(CUtensorMap* tm, const uint8_t* base, int W, int H, int npairs, long long stride,
