@@ -7,11 +7,8 @@
 // rank(dx,dy) = 1 + (dy+p)(2p+1) + (dx+p) otherwise (SAD <= 65280 and rank <= 4225 keep it in
 // 32 bits for B <= 16, p <= 32).
 //
-// One CTA per block.  The CTA stages the (B+2p) x (B+2p) edge-replicated window as four
-// byte-phase copies (copy k holds the window shifted left by k bytes), so any candidate row
-// is read as aligned 32-bit words; the current block sits in shared memory and is read by
-// broadcast.  Each thread owns a strided subset of the candidates; the CTA argmin is a
-// REDUX/CREDUX min over packed keys.
+// One CTA per tile of blocks: the tile's edge-replicated reference region is staged by TMA
+// (as for DCDS) and expanded into four byte-phase copies; see fs_kernel below.
 #pragma once
 #include <stdint.h>
 
@@ -20,85 +17,149 @@
 namespace me {
 
 struct FsArgs {
-    const uint8_t* cur0;
-    const uint8_t* ref0;
-    long long stride;
     int W, H, p;
+    int tbx, tby, ntx;      // tile of blocks per CTA, tiles per row
+    int pitch, rh;          // staged region (TMA box) width / rows
+    int cstride;            // bytes between byte-phase copies (cstride/4 = 8 mod 32 words)
+    int cur_off;            // byte offset of the current tile in shared memory
     int nbx, nb;
-    int lw;  // words per phase-copy row
+    int nch;                // dy chunks of B candidates: ceil((2p+1) / B)
     uint32_t* mv;
     uint32_t* sad;
     uint16_t* pts;
     unsigned long long* stats;
 };
 
+// One CTA per tile of blocks.  Thread items are (block, dx, chunk of B consecutive dy); a
+// thread keeps the current block in registers and streams the 2B-1 reference rows of its
+// chunk once, accumulating the SADs of all B candidates of the chunk (each reference row is
+// loaded once and reused by up to B candidates: W4 loads feed B*W4 VABSDIFF4).  Rows come
+// from the byte-phase copy (dx & 3) so they are aligned words; consecutive lanes take
+// consecutive dx, which the copy stride spreads over all 32 banks.  Per-block argmin:
+// shared-memory atomicMin on (SAD << 13 | rank) keys (reading C13).
 template <int B>
-__global__ void __launch_bounds__(256) fs_kernel(const FsArgs a) {
-    extern __shared__ __align__(16) uint8_t smem[];
+__global__ void __launch_bounds__(256)
+    fs_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
+              const FsArgs a) {
+    constexpr int W4 = B / 4;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint32_t s_key[64];
+    uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
     const int pair = blockIdx.y;
-    const int bi = blockIdx.x;
-    const int bx = (bi % a.nbx) * B, by = (bi / a.nbx) * B;
-    const uint8_t* cur = a.cur0 + (long long)pair * a.stride;
-    const uint8_t* ref = a.ref0 + (long long)pair * a.stride;
-    const int p = a.p, side = 2 * p + 1, nr = B + 2 * p, lw = a.lw;
-    uint32_t* win = reinterpret_cast<uint32_t*>(smem);  // [4][nr][lw]
-    uint32_t* cw = win + 4 * nr * lw;                   // [B][B/4]
-    __shared__ uint32_t red[8];
+    const int tx = blockIdx.x % a.ntx, ty = blockIdx.x / a.ntx;
+    const int TW = a.tbx * B, TH = a.tby * B;
+    const int x0 = tx * TW, y0 = ty * TH;
+    const int xs = (x0 - a.p) & ~15, ys = y0 - a.p;
+    const int pitch = a.pitch, p = a.p, side = 2 * p + 1;
+    uint8_t* sref = smem;
+    uint8_t* scur = smem + a.cur_off;
+    const int nby = a.nb / a.nbx;
+    const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, nby - ty * a.tby);
+    const int nbt = tbx_e * tby_e;
 
-    // stage the four phase copies: word (k, r, w) = bytes R(bx-p+4w+k+j, by-p+r), j = 0..3
-    for (int e = threadIdx.x; e < 4 * nr * lw; e += blockDim.x) {
-        const int k = e / (nr * lw);
-        const int rem = e - k * nr * lw;
-        const int r = rem / lw, w = rem - r * lw;
-        const int y = min(max(by - p + r, 0), a.H - 1);
-        const uint8_t* row = ref + (long long)y * a.W;
-        uint32_t v = 0;
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const int x = min(max(bx - p + 4 * w + k + j, 0), a.W - 1);
-            v |= (uint32_t)row[x] << (8 * j);
-        }
-        win[e] = v;
+    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    if (threadIdx.x < 64) s_key[threadIdx.x] = 0xffffffffu;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&s_bar, (uint32_t)(pitch * a.rh + TW * TH));
+        tma_load_3d(sref, &tm_ref, xs, ys, pair, &s_bar);
+        tma_load_3d(scur, &tm_cur, x0, y0, pair, &s_bar);
     }
-    for (int e = threadIdx.x; e < B * B / 4; e += blockDim.x) {
-        const int r = e / (B / 4), w = e - r * (B / 4);
-        cw[e] = *reinterpret_cast<const uint32_t*>(cur + (long long)(by + r) * a.W + bx + 4 * w);
+    mbar_wait(&s_bar, 0);
+    if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
+        fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
+    __syncthreads();
+    // byte-phase copies 1..3 of the region (copy k word q = region bytes 4q+k .. 4q+k+3)
+    {
+        const uint32_t* c0 = reinterpret_cast<const uint32_t*>(sref);
+        const int nw = pitch * a.rh / 4;
+        for (int q = threadIdx.x; q < nw; q += blockDim.x) {
+            const uint32_t lo = c0[q], hi = (q + 1 < nw) ? c0[q + 1] : 0u;
+#pragma unroll
+            for (int k = 1; k < 4; k++)
+                reinterpret_cast<uint32_t*>(sref + k * a.cstride)[q] = __funnelshift_r(lo, hi, 8 * k);
+        }
     }
     __syncthreads();
 
-    uint32_t key = 0xffffffffu;
-    for (int c = threadIdx.x; c < side * side; c += blockDim.x) {
-        const int dyp = c / side, dxp = c - dyp * side;  // dy+p, dx+p
-        const uint32_t* rw = win + (dxp & 3) * nr * lw + dyp * lw + (dxp >> 2);
-        uint32_t acc = 0;
+    const int nitem = nbt * side * a.nch;
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(sref);
+    const int cwords = a.cstride >> 2, pw = pitch >> 2;
+    for (int it = threadIdx.x; it < nitem; it += blockDim.x) {
+        const int per_blk = side * a.nch;
+        const int b = it / per_blk;
+        const int rem = it - b * per_blk;
+        const int c = rem / side;
+        const int dxp = rem - c * side;  // dx + p
+        const int lbx = b % tbx_e, lby = b / tbx_e;
+        uint32_t cw[B][W4];
 #pragma unroll
-        for (int i = 0; i < B; i++) {
+        for (int i = 0; i < B; i++)
 #pragma unroll
-            for (int w = 0; w < B / 4; w++) acc = vsad4(cw[i * (B / 4) + w], rw[i * lw + w], acc);
+            for (int w = 0; w < W4; w++)
+                cw[i][w] = reinterpret_cast<const uint32_t*>(scur + (lby * B + i) * TW + lbx * B)[w];
+        // candidate (dx, dy) block row i sits at region row lby*B + dy + p + i, column
+        // (x0 + lbx*B - p - xs) + dx + p
+        const int col = (x0 + lbx * B - p - xs) + dxp;
+        const uint32_t* base = sw + (col & 3) * cwords + (col >> 2);
+        const int row0 = lby * B + c * B;  // region row of (dy = c*B - p, i = 0)
+        const int nrow = a.rh;
+        uint32_t acc[B];
+#pragma unroll
+        for (int d = 0; d < B; d++) acc[d] = 0;
+#pragma unroll
+        for (int y = 0; y < 2 * B - 1; y++) {
+            const int rr = row0 + y;
+            uint32_t rw[W4];
+            if (rr < nrow) {
+#pragma unroll
+                for (int w = 0; w < W4; w++) rw[w] = base[rr * pw + w];
+            } else {
+#pragma unroll
+                for (int w = 0; w < W4; w++) rw[w] = 0;
+            }
+#pragma unroll
+            for (int d = 0; d < B; d++) {
+                const int i = y - d;
+                if (i >= 0 && i < B) {
+#pragma unroll
+                    for (int w = 0; w < W4; w++) acc[d] = vsad4(cw[i][w], rw[w], acc[d]);
+                }
+            }
         }
-        const uint32_t rank = (dxp == p && dyp == p) ? 0u : (uint32_t)(1 + c);
-        key = min(key, (acc << 13) | rank);
+        uint32_t key = 0xffffffffu;
+#pragma unroll
+        for (int d = 0; d < B; d++) {
+            const int dyp = c * B + d;  // dy + p
+            if (dyp < side) {
+                const uint32_t rank = (dxp == p && dyp == p) ? 0u : (uint32_t)(1 + dyp * side + dxp);
+                key = min(key, (acc[d] << 13) | rank);
+            }
+        }
+        atomicMin(&s_key[b], key);
     }
-    key = __reduce_min_sync(FULL, key);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        uint32_t k2 = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0xffffffffu;
-        k2 = __reduce_min_sync(FULL, k2);
+    // outputs + SSE at the FS MV (per-pair statistics), one warp per block
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int b = warp; b < nbt; b += nw) {
+        const uint32_t k2 = s_key[b];
         const uint32_t rank = k2 & 0x1fffu;
         const int cidx = rank == 0 ? p * side + p : (int)rank - 1;
         const int mdy = cidx / side - p, mdx = cidx % side - p;
-        // SSE of the block at the FS MV (for the per-pair statistics)
+        const int lbx = b % tbx_e, lby = b / tbx_e;
         uint32_t sse = 0;
-        const int dxp = mdx + p, dyp = mdy + p;
-        const uint32_t* rw = win + (dxp & 3) * nr * lw + dyp * lw + (dxp >> 2);
-        for (int e = threadIdx.x; e < B * B / 4; e += 32) {
-            const int r = e / (B / 4), w = e - r * (B / 4);
-            sse = ssd4(cw[e], rw[r * lw + w], sse);
+        const int col = (x0 + lbx * B - p - xs) + mdx + p;
+        const uint32_t* base = sw + (col & 3) * cwords + (col >> 2);
+        for (int e = lane; e < B * W4; e += 32) {
+            const int i = e / W4, w = e - i * W4;
+            const uint32_t cv = reinterpret_cast<const uint32_t*>(scur + (lby * B + i) * TW + lbx * B)[w];
+            sse = ssd4(cv, base[(lby * B + mdy + p + i) * pw + w], sse);
         }
         sse = __reduce_add_sync(FULL, sse);
-        if (threadIdx.x == 0) {
-            const long long g = (long long)pair * a.nb + bi;
+        if (lane == 0) {
+            const int bxg = x0 + lbx * B, byg = y0 + lby * B;
+            const long long g = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
             a.mv[g] = (uint32_t)(mdx & 0xffff) | ((uint32_t)mdy << 16);
             a.sad[g] = k2 >> 13;
             a.pts[g] = (uint16_t)(side * side);

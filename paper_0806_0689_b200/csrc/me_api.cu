@@ -208,18 +208,46 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
            int block, int p, int16_t* mv, uint32_t* sad, uint16_t* pts, uint64_t* stats,
            cudaStream_t s) {
     me::FsArgs a;
-    a.cur0 = cur0; a.ref0 = ref0; a.stride = stride;
+    const int B = block, nbx = W / B, nby = H / B, side = 2 * p + 1;
     a.W = W; a.H = H; a.p = p;
-    a.nbx = W / block; a.nb = a.nbx * (H / block);
-    a.lw = ((2 * p) >> 2) + block / 4 + 1;
+    a.nch = (side + B - 1) / B;
+    // tile: enough (block, dx, chunk) items for 256 threads, region <= 256 x 256 (TMA box)
+    int tbx = 1, tby = 1;
+    while (tbx * tby * side * a.nch < 1024 && tbx * tby < 64) {
+        if (tbx <= tby && (tbx * 2) * B + 2 * p + 31 <= 240) tbx *= 2;
+        else if ((tby * 2) * B + 2 * p <= 256) tby *= 2;
+        else break;
+    }
+    tbx = std::min(tbx, nbx);
+    tby = std::min(tby, nby);
+    if ((tbx * B) % 16) tbx = std::min(nbx, ((tbx * B + 15) / 16) * 16 / B);
+    a.tbx = tbx; a.tby = tby;
+    a.ntx = (nbx + tbx - 1) / tbx;
+    const int nty = (nby + tby - 1) / tby;
+    const int TW = tbx * B, TH = tby * B;
+    a.pitch = ((TW + 2 * p + 31) + 15) & ~15;
+    a.rh = TH + 2 * p;
+    const int rbytes = a.pitch * a.rh;
+    // copy stride: >= region, 128-aligned copy 0, stride/4 = 8 (mod 32) words spreads the copies
+    int cs = (rbytes + 127) & ~127;
+    while (((cs / 4) & 31) != 8) cs += 16;
+    a.cstride = cs;
+    a.cur_off = (4 * cs + 127) & ~127;
+    a.nbx = nbx; a.nb = nbx * nby;
     a.mv = reinterpret_cast<uint32_t*>(mv); a.sad = sad; a.pts = pts;
     a.stats = reinterpret_cast<unsigned long long*>(stats);
-    const size_t smem = (size_t)4 * (block + 2 * p) * a.lw * 4 + (size_t)block * block;
-    if ((int)smem > g_smem_optin - 64) return fail(ME_EINVAL, "FS window does not fit in shared memory");
+    const size_t smem = 128 + (size_t)a.cur_off + (size_t)TW * TH;
+    if ((int)smem > g_smem_optin - 1024) return fail(ME_EINVAL, "FS tile does not fit in shared memory");
+    if (tbx * tby > 64) return fail(ME_EINVAL, "FS tile too large");
+    CUtensorMap tc, tr;
+    int rc = make_tmap(&tc, cur0, W, H, npairs, stride, TW, TH);
+    if (rc) return rc;
+    rc = make_tmap(&tr, ref0, W, H, npairs, stride, a.pitch, a.rh);
+    if (rc) return rc;
     if (stats) CK(cudaMemsetAsync(stats, 0, sizeof(uint64_t) * 3 * (size_t)npairs, s));
-    dim3 grid(a.nb, npairs);
-    if (block == 16) me::fs_kernel<16><<<grid, 256, smem, s>>>(a);
-    else me::fs_kernel<8><<<grid, 256, smem, s>>>(a);
+    dim3 grid(a.ntx * nty, npairs);
+    if (block == 16) me::fs_kernel<16><<<grid, 256, smem, s>>>(tc, tr, a);
+    else me::fs_kernel<8><<<grid, 256, smem, s>>>(tc, tr, a);
     g_launches++;
     CK(cudaGetLastError());
     return ME_OK;
