@@ -41,7 +41,7 @@ UNIT = "blocks/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -71,27 +71,40 @@ REASON_BITS = {
 
 
 class ClockSampler:
+    """nvidia-smi sampler started before the timed region; only samples taken between
+    mark_start() and mark_end() are summarised (nvidia-smi needs ~0.5 s to start)."""
+
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 5.0
+            while not self.lines and time.time() < deadline:
+                time.sleep(0.02)
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def __exit__(self, *a):
         if self.proc:
@@ -103,7 +116,13 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], [], set()
-        for ln in self.lines:
+        lines = self.lines
+        if self.t0 is not None and self.t1 is not None:
+            inside = [x for x in lines if self.t0 <= x[0] <= self.t1]
+            if not inside and lines:  # region shorter than the sampling period: nearest sample
+                inside = [min(lines, key=lambda x: abs(x[0] - (self.t0 + self.t1) / 2))]
+            lines = inside
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 4:
                 continue
@@ -245,16 +264,17 @@ def main():
         me.me_dcds_batch(frames, cfg.B, cfg.p, mv, sad, pts, st)
         gather()
 
-    for _ in range(max(args.warmup, 0)):
-        step()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    launches0 = me.me_launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk:  # started first: warm-up steps also bring clocks up
+        for _ in range(max(args.warmup, 0)):
+            step()
         torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        launches0 = me.me_launch_count()
+        torch.cuda.synchronize()
+        clk.mark_start()
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
@@ -265,6 +285,7 @@ def main():
             gather()
         t_end.record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
     launches = me.me_launch_count() - launches0
     total_ms = t_start.elapsed_time(t_end)
     kern_ms = [a.elapsed_time(b) for a, b in ev]
