@@ -92,6 +92,7 @@ struct DcdsLaunch {
     dim3 grid;
     size_t smem;
     int G;
+    int NW;  // warps per CTA
     int TW, TH;
 };
 
@@ -102,9 +103,16 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     me::SearchArgs& a = L.a;
     const int nbx = W / B, nby = H / B;
     L.G = (B == 16) ? 8 : 2;
+    L.NW = (B == 16) ? 8 : 4;
+    if (const char* e = getenv("ME_NW")) {
+        const int nw = atoi(e);
+        if (nw == 2 || nw == 4 || nw == 8) L.NW = nw;
+    }
 
+    // measured on B200 (profiles/r1/SUMMARY.md): B=8: G=2, 4 warps, 16x4 blocks;
+    // B=16: G=8, 8 warps, 8x4 blocks
     int tbx = (B == 16) ? 8 : 16;
-    int tby = (B == 16) ? 2 : 4;  // measured on B200 (profiles/r1/TUNING.md)
+    int tby = 4;
     if (const char* e = getenv("ME_G")) {
         const int g = atoi(e);
         if (g == 1 || g == 2 || g == 4 || g == 8) L.G = g;
@@ -134,7 +142,7 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     a.nb = nbx * nby;
     L.grid = dim3(a.ntx * nty, npairs);
     for (int i = 0; i < 8; i++) a.pcode[i] = me::pat_code(i);
-    const int groups = kNWarp * 32 / L.G;
+    const int groups = L.NW * 32 / L.G;
     a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;  // TMA destinations are 128-byte aligned
     L.TW = TW; L.TH = TH;
     L.smem = 128 + (size_t)a.cur_off + (size_t)TW * TH + (size_t)groups * a.bm_words * 4 + 32;
@@ -143,7 +151,9 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
 
 template <int B, int G, int VARIANT>
 void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap& tr, cudaStream_t s) {
-    me::dcds_kernel<B, G, kNWarp, VARIANT><<<L.grid, kNWarp * 32, L.smem, s>>>(tc, tr, L.a);
+    if (L.NW == 2) me::dcds_kernel<B, G, 2, VARIANT><<<L.grid, 64, L.smem, s>>>(tc, tr, L.a);
+    else if (L.NW == 8) me::dcds_kernel<B, G, 8, VARIANT><<<L.grid, 256, L.smem, s>>>(tc, tr, L.a);
+    else me::dcds_kernel<B, G, 4, VARIANT><<<L.grid, 128, L.smem, s>>>(tc, tr, L.a);
 }
 
 template <int B, int VARIANT>
@@ -312,7 +322,9 @@ int me_init(int device) {
     g_smem_optin = (int)prop.sharedMemPerBlockOptin;
     int rc;
 #define ME_ALLOW(B, G, V) \
-    if ((rc = allow_smem(me::dcds_kernel<B, G, kNWarp, V>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<B, G, 2, V>))) return rc;             \
+    if ((rc = allow_smem(me::dcds_kernel<B, G, 4, V>))) return rc;             \
+    if ((rc = allow_smem(me::dcds_kernel<B, G, 8, V>))) return rc;
     ME_DCDS_KERNELS(ME_ALLOW)
 #undef ME_ALLOW
     if ((rc = allow_smem(me::fs_kernel<16>))) return rc;
