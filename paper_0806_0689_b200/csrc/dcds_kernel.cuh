@@ -199,119 +199,57 @@ inline constexpr uint32_t pat_code(int pid) {  // host side (kernel args)
 __device__ __forceinline__ int code_dx(uint32_t w, int k) { return (int)((w >> (6 * k)) & 7u) - 2; }
 __device__ __forceinline__ int code_dy(uint32_t w, int k) { return (int)((w >> (6 * k + 3)) & 7u) - 2; }
 
-template <int B, int G, int NWARP, int VARIANT>
-__global__ void __launch_bounds__(NWARP * 32)
-    dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
-                const SearchArgs a) {
-    static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "lane-group size");
-    constexpr int R = B / G;      // rows per lane (lane j of a group: rows j, j+G, ...)
-    constexpr int W4 = B / 4;     // 32-bit words per block row
-    constexpr int NG = 32 / G;    // groups per warp
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    __shared__ int4 s_poff[8];
-    __shared__ uint32_t s_pcode[8];
-    __shared__ __align__(8) uint64_t s_bar;
-    uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int j = lane % G, g = lane / G, leader = g * G;
-    const int pair = blockIdx.y;
-    const int tx = blockIdx.x % a.ntx, ty = blockIdx.x / a.ntx;
-    const int TW = a.tbx * B, TH = a.tby * B;
-    const int x0 = tx * TW, y0 = ty * TH;
-    const int xs = (x0 - a.p) & ~15;  // floor to 16 (two's complement)
-    const int ys = y0 - a.p;
-    const int pitch = a.pitch, p = a.p;
-
-    // shared layout: reference region (pitch x rh) | current tile (TW x TH) | bitmaps | stats
-    uint8_t* sref = smem;
-    uint8_t* scur = smem + a.cur_off;
-    uint32_t* bms = reinterpret_cast<uint32_t*>(scur + TW * TH);
-    uint32_t* bm = bms + (warp * NG + g) * a.bm_words;
-    int* ctr = reinterpret_cast<int*>(bms + NWARP * NG * a.bm_words);
-
-    // ---- stage the tile with TMA: reference region + current tile, one mbarrier
-    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        mbar_expect_tx(&s_bar, (uint32_t)(pitch * a.rh + TW * TH));
-        tma_load_3d(sref, &tm_ref, xs, ys, pair, &s_bar);
-        tma_load_3d(scur, &tm_cur, x0, y0, pair, &s_bar);
-    }
-    if (threadIdx.x == 0) *ctr = 0;
-    if (threadIdx.x < 8) {
-        const uint32_t w = a.pcode[threadIdx.x];
-        s_pcode[threadIdx.x] = w;
-        s_poff[threadIdx.x] = make_int4(code_dy(w, 0) * pitch + code_dx(w, 0),
-                                        code_dy(w, 1) * pitch + code_dx(w, 1),
-                                        code_dy(w, 2) * pitch + code_dx(w, 2),
-                                        code_dy(w, 3) * pitch + code_dx(w, 3));
-    }
-    mbar_wait(&s_bar, 0);
-    if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
-        fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
-    __syncthreads();
-
-    const uint32_t* s = reinterpret_cast<const uint32_t*>(sref);
-    const int rstride = G * pitch;  // bytes between a lane's rows
-    const int jrow = j * pitch;     // byte offset of the lane's first row
-    const int nby = a.nb / a.nbx;
-    const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, nby - ty * a.tby);
-    const int nbt = tbx_e * tby_e;
-    const float inv_tbx = 1.0f / (float)tbx_e;
-
-    // group state (every lane of a group holds the same values)
+// ----------------------------------------------------------------------------------------
+// One group pass (all lanes of the warp call it; every group advances its own state).
+// ----------------------------------------------------------------------------------------
+template <int B, int G>
+struct GroupState {
+    static constexpr int R = B / G;   // rows per lane (lane j of a group: rows j, j+G, ...)
+    static constexpr int W4 = B / 4;  // 32-bit words per block row
     int st = ST_DONE, pid = 0, kind = 0, cx = 0, cy = 0, pts = 0, want = 3;
     int bofs = 0, cpos = 0;
-    long long gblk = 0;
     uint32_t best = 0, s0 = 0, key1 = 0xffffffffu;
     uint32_t cw[R][W4];
-#pragma unroll
-    for (int r = 0; r < R; r++)
-#pragma unroll
-        for (int w = 0; w < W4; w++) cw[r][w] = 0;
-    unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
 
-    for (;;) {
-        // ---- groups that are done take the next block of the tile
-        const bool need = (st == ST_DONE);
-        const unsigned ball = __ballot_sync(FULL, need && j == 0);
-        if (ball) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(ctr, __popc(ball));
-            base = __shfl_sync(FULL, base, 0);
-            int idx = base + __popc(ball & ((1u << lane) - 1u));
-            idx = __shfl_sync(FULL, idx, leader);
-            if (need) {
-                if (idx < nbt) {
-                    // idx / tbx_e in float is exact here: idx < 2^16, tbx_e <= 2^8
-                    const int lby = (int)(((float)idx + 0.5f) * inv_tbx);
-                    const int lbx = idx - lby * tbx_e;
-                    const int bxg = x0 + lbx * B, byg = y0 + lby * B;
-                    bofs = (byg - ys) * pitch + (bxg - xs);
-                    cpos = bofs;
-                    gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
+    // Start the search of the block whose (0,0) candidate is at byte `origin` of the staged
+    // region and whose current rows are at `crow0` (row stride `cpitch`): load the lane's
+    // current rows, clear the group's visited bitmap (reading C5), enter Step 1.
+    __device__ __forceinline__ void start(int origin, const uint8_t* crow0, int cpitch, int j,
+                                          uint32_t* bm, int bm_words) {
+        bofs = origin;
+        cpos = origin;
 #pragma unroll
-                    for (int r = 0; r < R; r++) {
-                        const uint32_t* crow = reinterpret_cast<const uint32_t*>(
-                            scur + (lby * B + j + G * r) * TW + lbx * B);
+        for (int r = 0; r < R; r++) {
+            const uint32_t* crow = reinterpret_cast<const uint32_t*>(crow0 + (j + G * r) * cpitch);
 #pragma unroll
-                        for (int w = 0; w < W4; w++) cw[r][w] = crow[w];
-                    }
-                    for (int w = j * 4; w < a.bm_words; w += 4 * G)
-                        *reinterpret_cast<uint4*>(bm + w) = make_uint4(0, 0, 0, 0);
-                    st = ST_S1A; pid = 0; kind = 0; cx = 0; cy = 0; pts = 0; want = 3;
-                    key1 = 0xffffffffu;
-                } else {
-                    st = ST_IDLE;
-                }
-            }
-            __syncwarp();
+            for (int w = 0; w < W4; w++) cw[r][w] = crow[w];
         }
-        if (__all_sync(FULL, st == ST_IDLE)) break;
+        for (int w = j * 4; w < bm_words; w += 4 * G)
+            *reinterpret_cast<uint4*>(bm + w) = make_uint4(0, 0, 0, 0);
+        st = ST_S1A; pid = 0; kind = 0; cx = 0; cy = 0; pts = 0; want = 3;
+        key1 = 0xffffffffu;
+    }
 
+    // SSE (P:342 aspect 4) of this lane's rows at the current centre.
+    __device__ __forceinline__ uint32_t sse_rows(const uint32_t* s, int jrow, int rstride) const {
+        uint32_t rw[R][W4];
+        ref_rows<R, W4>(s, cpos + jrow, rstride, rw);
+        uint32_t ss = 0;
+#pragma unroll
+        for (int r = 0; r < R; r++)
+#pragma unroll
+            for (int w = 0; w < W4; w++) ss = ssd4(cw[r][w], rw[r][w], ss);
+        return ss;
+    }
+
+    // One pass of the group's state machine; returns true when the block's search ended.
+    template <int VARIANT>
+    __device__ __forceinline__ bool pass(const uint32_t* s, uint32_t* bm, const uint32_t* s_pcode,
+                                         const int4* s_poff, int j, int leader, int p, int pitch,
+                                         int rstride, int jrow) {
         const uint32_t pw = s_pcode[pid];
         const int4 po = s_poff[pid];
-        const uint32_t used = (st == ST_IDLE) ? 0u : ((pw >> 24) & (st == ST_S4 ? (uint32_t)want : 0xfu));
+        const uint32_t used = (st >= ST_IDLE || st == ST_DONE) ? 0u : ((pw >> 24) & (st == ST_S4 ? (uint32_t)want : 0xfu));
 
         // ---- visited-set test-and-set (reading C5): lane j of a group owns slots j, j+G, ...
         unsigned m4 = 0;
@@ -423,29 +361,118 @@ __global__ void __launch_bounds__(NWARP * 32)
             fin = true;
         }
 
+        return fin;
+    }
+};
+
+template <int B, int G, int NWARP, int VARIANT>
+__global__ void __launch_bounds__(NWARP * 32)
+    dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
+                const SearchArgs a) {
+    static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "lane-group size");
+    constexpr int R = B / G;      // rows per lane (lane j of a group: rows j, j+G, ...)
+    constexpr int W4 = B / 4;     // 32-bit words per block row
+    constexpr int NG = 32 / G;    // groups per warp
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ int4 s_poff[8];
+    __shared__ uint32_t s_pcode[8];
+    __shared__ __align__(8) uint64_t s_bar;
+    uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane % G, g = lane / G, leader = g * G;
+    const int pair = blockIdx.y;
+    const int tx = blockIdx.x % a.ntx, ty = blockIdx.x / a.ntx;
+    const int TW = a.tbx * B, TH = a.tby * B;
+    const int x0 = tx * TW, y0 = ty * TH;
+    const int xs = (x0 - a.p) & ~15;  // floor to 16 (two's complement)
+    const int ys = y0 - a.p;
+    const int pitch = a.pitch, p = a.p;
+
+    // shared layout: reference region (pitch x rh) | current tile (TW x TH) | bitmaps | stats
+    uint8_t* sref = smem;
+    uint8_t* scur = smem + a.cur_off;
+    uint32_t* bms = reinterpret_cast<uint32_t*>(scur + TW * TH);
+    uint32_t* bm = bms + (warp * NG + g) * a.bm_words;
+    int* ctr = reinterpret_cast<int*>(bms + NWARP * NG * a.bm_words);
+
+    // ---- stage the tile with TMA: reference region + current tile, one mbarrier
+    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&s_bar, (uint32_t)(pitch * a.rh + TW * TH));
+        tma_load_3d(sref, &tm_ref, xs, ys, pair, &s_bar);
+        tma_load_3d(scur, &tm_cur, x0, y0, pair, &s_bar);
+    }
+    if (threadIdx.x == 0) *ctr = 0;
+    if (threadIdx.x < 8) {
+        const uint32_t w = a.pcode[threadIdx.x];
+        s_pcode[threadIdx.x] = w;
+        s_poff[threadIdx.x] = make_int4(code_dy(w, 0) * pitch + code_dx(w, 0),
+                                        code_dy(w, 1) * pitch + code_dx(w, 1),
+                                        code_dy(w, 2) * pitch + code_dx(w, 2),
+                                        code_dy(w, 3) * pitch + code_dx(w, 3));
+    }
+    mbar_wait(&s_bar, 0);
+    if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
+        fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
+    __syncthreads();
+
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(sref);
+    const int rstride = G * pitch;  // bytes between a lane's rows
+    const int jrow = j * pitch;     // byte offset of the lane's first row
+    const int nby = a.nb / a.nbx;
+    const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, nby - ty * a.tby);
+    const int nbt = tbx_e * tby_e;
+    const float inv_tbx = 1.0f / (float)tbx_e;
+
+    GroupState<B, G> gs;  // group state (every lane of a group holds the same values)
+    long long gblk = 0;
+    unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
+
+    for (;;) {
+        // ---- groups that are done take the next block of the tile
+        const bool need = (gs.st == ST_DONE);
+        const unsigned ball = __ballot_sync(FULL, need && j == 0);
+        if (ball) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(ctr, __popc(ball));
+            base = __shfl_sync(FULL, base, 0);
+            int idx = base + __popc(ball & ((1u << lane) - 1u));
+            idx = __shfl_sync(FULL, idx, leader);
+            if (need) {
+                if (idx < nbt) {
+                    // idx / tbx_e in float is exact here: idx < 2^16, tbx_e <= 2^8
+                    const int lby = (int)(((float)idx + 0.5f) * inv_tbx);
+                    const int lbx = idx - lby * tbx_e;
+                    const int bxg = x0 + lbx * B, byg = y0 + lby * B;
+                    gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
+                    gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW,
+                             j, bm, a.bm_words);
+                } else {
+                    gs.st = ST_IDLE;
+                }
+            }
+            __syncwarp();
+        }
+        if (__all_sync(FULL, gs.st == ST_IDLE)) break;
+
+        const bool fin = gs.template pass<VARIANT>(s, bm, s_pcode, s_poff, j, leader, p, pitch, rstride, jrow);
+
         // ---- finished blocks: SSE of the compensated block (P:342 aspect 4), outputs
         if (__any_sync(FULL, fin)) {
-            uint32_t ss = 0;
-            if (fin) {  // only finishing groups read shared memory
-                uint32_t rw[R][W4];
-                ref_rows<R, W4>(s, cpos + jrow, rstride, rw);
-#pragma unroll
-                for (int r = 0; r < R; r++)
-#pragma unroll
-                    for (int w = 0; w < W4; w++) ss = ssd4(cw[r][w], rw[r][w], ss);
-            }
+            uint32_t ss = fin ? gs.sse_rows(s, jrow, rstride) : 0u;  // finishing groups only
 #pragma unroll
             for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
             if (fin) {
                 if (j == 0) {
-                    a.mv[gblk] = (uint32_t)(cx & 0xffff) | ((uint32_t)cy << 16);
-                    a.sad[gblk] = best;
-                    a.pts[gblk] = (uint16_t)pts;
-                    acc_pts += (unsigned)pts;
-                    acc_sad += best;
+                    a.mv[gblk] = (uint32_t)(gs.cx & 0xffff) | ((uint32_t)gs.cy << 16);
+                    a.sad[gblk] = gs.best;
+                    a.pts[gblk] = (uint16_t)gs.pts;
+                    acc_pts += (unsigned)gs.pts;
+                    acc_sad += gs.best;
                     acc_sse += ss;
                 }
-                st = ST_DONE;
+                gs.st = ST_DONE;
             }
         }
     }
