@@ -105,6 +105,15 @@ int me_fullsearch_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_s
 int me_mc_sse_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
                     int W, int H, int block, const int16_t* mv, uint64_t* sse_out);
 
+/* Table-IX-style quality of a motion field against the full-search field (P:342 aspects 5
+ * and 6): for each of npairs pairs of nb blocks, out[2k] = number of blocks
+ * whose MV equals the FS MV (the "probability of finding the true MV" times nb) and
+ * out[2k+1] = sum over blocks of the Euclidean distance |mv - mv_fs| (double; deterministic
+ * fixed-order reduction).  mv, mv_fs: device [npairs][nb][2] int16; out: device double
+ * [npairs][2], overwritten.  MAD, MSE, NSP and PSNR follow from the stats_out of the searches
+ * (MAD = sum SAD / (nb*B*B), MSE = SSE / (W*H), NSP = sum points / nb). */
+int me_quality_batch(const int16_t* mv, const int16_t* mv_fs, int npairs, int nb, double* out);
+
 /* End-to-end variant of me_dcds_batch on HOST buffers: frames (host, [npairs] x
  * pair_stride bytes as above) are copied to the device in chunks on two streams,
  * overlapped with the search of the previous chunk, and the outputs (host) copied back.

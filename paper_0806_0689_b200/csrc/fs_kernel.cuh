@@ -206,4 +206,46 @@ __global__ void __launch_bounds__(256) mc_sse_kernel(const McArgs a) {
     if (lane == 0) atomicAdd(&a.sse[pair], (unsigned long long)s);
 }
 
+// Table-IX-style quality of a motion field against the FS field (P:342 aspects 5 and 6):
+// per pair, the number of blocks whose MV equals the FS MV and the sum of the Euclidean
+// distances |mv - mv_fs| (double).  One CTA per pair; each thread sums a fixed strided subset
+// of the blocks and the CTA reduces in a fixed order, so the result is deterministic.
+__global__ void __launch_bounds__(256) quality_kernel(const uint32_t* mv, const uint32_t* mv_fs,
+                                                      int nb, double* out) {
+    const int pair = blockIdx.x;
+    const uint32_t* m = mv + (long long)pair * nb;
+    const uint32_t* f = mv_fs + (long long)pair * nb;
+    double dsum = 0.0;
+    unsigned hits = 0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+        const uint32_t a = m[i], b = f[i];
+        const int dx = (int)(int16_t)(a & 0xffff) - (int)(int16_t)(b & 0xffff);
+        const int dy = (int)(int16_t)(a >> 16) - (int)(int16_t)(b >> 16);
+        hits += (a == b);
+        dsum += sqrt((double)(dx * dx + dy * dy));
+    }
+    __shared__ double sd[8];
+    __shared__ unsigned sh[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dsum += __shfl_xor_sync(FULL, dsum, o);
+        hits += __shfl_xor_sync(FULL, hits, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sd[threadIdx.x >> 5] = dsum;
+        sh[threadIdx.x >> 5] = hits;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double d = 0.0;
+        unsigned h = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            d += sd[w];
+            h += sh[w];
+        }
+        out[2 * pair] = (double)h;
+        out[2 * pair + 1] = d;
+    }
+}
+
 }  // namespace me

@@ -424,6 +424,18 @@ int me_mc_psnr(const uint8_t* cur, const uint8_t* ref, int W, int H, int block, 
     return ME_OK;
 }
 
+int me_quality_batch(const int16_t* mv, const int16_t* mv_fs, int npairs, int nb, double* out) {
+    if (!mv || !mv_fs || !out) return fail(ME_EINVAL, "NULL pointer");
+    if (npairs < 1 || nb < 1 || npairs > 65535) return fail(ME_EINVAL, "bad npairs / nb");
+    if (!aligned(mv, 4) || !aligned(mv_fs, 4) || !aligned(out, 8)) return fail(ME_EALIGN, "misaligned pointer");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    me::quality_kernel<<<npairs, 256, 0, g_stream>>>(reinterpret_cast<const uint32_t*>(mv),
+                                                     reinterpret_cast<const uint32_t*>(mv_fs), nb, out);
+    g_launches++;
+    CK(cudaGetLastError());
+    return ME_OK;
+}
+
 int me_dcds_batch_host(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
                        int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
                        uint16_t* points_out, uint64_t* stats_out) {

@@ -20,7 +20,7 @@ ME_OK, ME_EINVAL, ME_EALIGN, ME_ENOTINIT, ME_ECUDA, ME_ENOMEM = 0, -1, -2, -3, -
 SYMBOLS = (
     "me_init", "me_set_stream", "me_dcds", "me_fullsearch", "me_mc_psnr", "me_dcds_batch",
     "me_dcds_s_batch", "me_fullsearch_batch", "me_mc_sse_batch", "me_dcds_batch_host",
-    "me_launch_count", "me_strerror", "me_shutdown",
+    "me_launch_count", "me_strerror", "me_shutdown", "me_quality_batch",
 )
 
 
@@ -55,6 +55,7 @@ def load() -> ctypes.CDLL:
     L.me_fullsearch_batch.argtypes = batch
     L.me_dcds_batch_host.argtypes = batch
     L.me_mc_sse_batch.argtypes = [vp, vp, i64, i32, i32, i32, i32, vp, vp]
+    L.me_quality_batch.argtypes = [vp, vp, i32, i32, vp]
     L.me_launch_count.argtypes = []
     L.me_launch_count.restype = i64
     L.me_strerror.argtypes = [i32]
@@ -164,6 +165,15 @@ def me_mc_sse_batch(frames, block, mv, sse):
     n, _, H, W = frames.shape
     base = _ptr(frames)
     _check(load().me_mc_sse_batch(base, base + H * W, 2 * H * W, n, W, H, block, _ptr(mv), _ptr(sse)))
+
+
+def me_quality_batch(mv, mv_fs, out=None):
+    """Per pair (hits, sum of Euclidean distances) of mv against mv_fs ([n, nb, 2] int16)."""
+    n, nb = mv.shape[0], mv.shape[1]
+    if out is None:
+        out = torch.empty(n, 2, dtype=torch.float64, device=mv.device)
+    _check(load().me_quality_batch(_ptr(mv), _ptr(mv_fs), n, nb, _ptr(out)))
+    return out
 
 
 def me_launch_count() -> int:

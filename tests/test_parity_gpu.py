@@ -301,3 +301,31 @@ def test_nccl_gather_single_rank():
             assert torch.equal(a, b)
     finally:
         dist.destroy_process_group()
+
+
+def test_quality_kernel_examples_and_parity():
+    """me_quality_batch: S:480-488 examples (field vs itself -> (0, 1); one of two blocks off by
+    (1,0) -> (0.5, 0.5); all off by (3,4) -> (5, 0)) and c1 DCDS-vs-FS against numpy."""
+    z = torch.zeros(1, 2, 2, dtype=torch.int16, device=DEV)
+    one = z.clone()
+    one[0, 1, 0] = 1
+    far = z.clone()
+    far[..., 0] = 3
+    far[..., 1] = 4
+    q = me.me_quality_batch(torch.cat([z, one, far]), torch.cat([z, z, z])).cpu().numpy()
+    np.testing.assert_allclose(q[:, 0] / 2, [1.0, 0.5, 0.0])
+    np.testing.assert_allclose(q[:, 1] / 2, [0.0, 0.5, 5.0], rtol=1e-15)
+    cfg = synth.CONFIGS["c1"]
+    fr = synth.make_sequence(cfg, device=DEV)
+    mv, _, _, _ = gpu_search(fr, cfg.B, cfg.p)
+    fmv, _, _, _ = gpu_search(fr, cfg.B, cfg.p, "fs")
+    q = me.me_quality_batch(torch.from_numpy(mv).to(DEV), torch.from_numpy(fmv).to(DEV)).cpu().numpy()
+    d = (mv.astype(np.int64) - fmv.astype(np.int64))
+    hits = (d == 0).all(2).sum(1)
+    dist = np.sqrt((d ** 2).sum(2)).sum(1)
+    np.testing.assert_array_equal(q[:, 0], hits)
+    np.testing.assert_allclose(q[:, 1], dist, rtol=1e-12)
+    from paper_0806_0689_b200 import report
+    rep = report.compare_dcds_fs(fr, cfg.B, cfg.p)
+    assert rep["FS"]["prob"] == 1.0 and rep["FS"]["dist"] == 0.0 and rep["FS"]["nsp"] == 225.0
+    assert rep["FS"]["mad"] <= rep["DCDS"]["mad"] and rep["DCDS"]["nsp"] < 225.0
