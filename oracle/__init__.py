@@ -119,6 +119,21 @@ def _search(fn, cur, ref, B, p, *extra):
     return mv[:nb], sad_[:nb], pts[:nb]
 
 
+# Algorithm ids of the C oracle (oracle.h): DCDS, DCDS^S and the paper's comparison
+# BMAs on the same machinery (readings C23-C26).
+ALGS = {"dcds": 0, "dcds_s": 1, "cds": 2, "ds": 3, "hexbs_h": 4, "hexbs_v": 5}
+
+
+def bma(cur, ref, B, p, alg: str):
+    """Any block-matching search of :data:`ALGS` over every block: (mv, sad, points)."""
+    return dcds(cur, ref, B, p, ALGS[alg])
+
+
+def bma_block(cur, ref, B, p, bx, by, alg: str):
+    """Single-block version of :func:`bma`: ((dx, dy), sad, points)."""
+    return dcds_block(cur, ref, B, p, bx, by, ALGS[alg])
+
+
 def dcds(cur, ref, B, p, variant: int = 0):
     """DCDS over every block: returns (mv[nb,2] int16, sad[nb] u32, points[nb] u16)."""
     return _search(lib().oracle_dcds, cur, ref, B, p, variant)

@@ -96,7 +96,26 @@ static const int VDSP[4][2] = {{-1, 0}, {1, 0}, {0, -2}, {0, 2}};
 static const int HMID[2][2] = {{-1, 0}, {1, 0}};
 static const int VMID[2][2] = {{0, -1}, {0, 1}};
 
-enum { KIND_HCSP = 0, KIND_HDSP = 1, KIND_VDSP = 2, KIND_MID = 3 };
+enum { KIND_HCSP = 0, KIND_HDSP = 1, KIND_VDSP = 2, KIND_MID = 3, KIND_LDSP = 4, KIND_SDSP = 5,
+       KIND_CSP = 6, KIND_HEX = 7 };
+
+/* Competitor searches (the paper's comparison BMAs, Table VII
+ * P:307-324).  Their source papers ([10] DS, [12] HEXBS, [13] CDS) are not in the container;
+ * the patterns and steps below are the readings DESIGN.md lists (C23-C26), pinned by the
+ * Table VII CDS and DS blocks (64/64 each), Fig. 3 / Table VI (pattern geometry) and
+ * Table VIII distribution 2.  Same machinery as DCDS: visited set, strict compare.  Point
+ * order (reading C26): ascending distance from the pattern centre, ties by the C7 key
+ * (|dy|,|dx|,dy,dx) -- Table VII's DS block rejects the plain C7 order.                 */
+/* Large diamond (DS [10]): the four diagonal neighbours, then the distance-2 vertices.  */
+static const int LDSP[8][2] = {{-1, -1}, {1, -1}, {-1, 1}, {1, 1}, {-2, 0}, {2, 0}, {0, -2}, {0, 2}};
+/* Small diamond: the four distance-1 points (DS / CDS final step, HEXBS final step).    */
+static const int SDSP[4][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}};
+/* 5x5 cross (CDS [13] first step; Table VI "5x5 cross search pattern in CDS", 9 points). */
+static const int CSP[8][2] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}, {-2, 0}, {2, 0}, {0, -2}, {0, 2}};
+/* Horizontal hexagon (h-HEXBS [12], Fig. 2a; Table VI 0.6457/7) and its vertical
+ * counterpart (v-HEXBS, Fig. 2b).                                                  */
+static const int HEXH[6][2] = {{-2, 0}, {2, 0}, {-1, -2}, {1, -2}, {-1, 2}, {1, 2}};
+static const int HEXV[6][2] = {{0, -2}, {0, 2}, {-2, -1}, {2, -1}, {-2, 1}, {2, 1}};
 
 typedef double (*cost_fn)(int dx, int dy, void* ctx);
 
@@ -208,6 +227,92 @@ static void dcds_search(search_t* s, int variant, int* mvx, int* mvy, double* be
     *mvx = bx; *mvy = by; *best = bs;
 }
 
+/* DS (ref. [10]): the large diamond repeated, recentred on the BMP, until the BMP is
+ * its centre; then the small diamond once; the final BMP is the MV (reading C24).  Also the
+ * Step 3-4 of CDS. */
+static void ds_from(search_t* s, int step, int* bx, int* by, double* bs) {
+    int cx = *bx, cy = *by;
+    for (;;) {
+        scan(s, cx, cy, LDSP, 8, step++, KIND_LDSP, bx, by, bs);
+        if (*bx == cx && *by == cy) break;
+        cx = *bx; cy = *by;
+    }
+    scan(s, cx, cy, SDSP, 4, step, KIND_SDSP, bx, by, bs);
+}
+
+static void ds_search(search_t* s, int* mvx, int* mvy, double* best) {
+    double s0;
+    score(s, 0, 0, 0, KIND_LDSP, &s0);
+    int bx = 0, by = 0;
+    double bs = s0;
+    ds_from(s, 0, &bx, &by, &bs);
+    *mvx = bx; *mvy = by; *best = bs;
+}
+
+/* CDS (ref. [13]; reading C23): Step 1 the 9-point 5x5 cross at the origin, stop if the
+ * centre is the BMP (first-step stop).  Step 2: the two unchecked points of the central 3x3
+ * square beside the arm of the BMP m (arm along x with sign s: (s,-1), (s,1); along y:
+ * (-1,s), (1,s)); the central 3x3 square is preferred, so a tie with m moves the BMP there
+ * (Table VII's CDS block requires it, e.g. (2,1) -> 17).  If m was a distance-1 arm point and
+ * stays the BMP, stop (second-step stop).  Steps 3-4: DS (large diamond until centred,
+ * then the small diamond) from the BMP. */
+static void cds_search(search_t* s, int* mvx, int* mvy, double* best) {
+    double s0;
+    score(s, 0, 0, 0, KIND_CSP, &s0);
+    int bx = 0, by = 0;
+    double bs = s0;
+    scan(s, 0, 0, CSP, 8, 0, KIND_CSP, &bx, &by, &bs);
+    if (bx == 0 && by == 0) { *mvx = 0; *mvy = 0; *best = bs; return; }
+    const int mx = bx, my = by;
+    const int sg = (mx + my) > 0 ? 1 : -1;  /* sign of the arm (one of mx, my is 0) */
+    int pair[2][2];
+    if (my == 0) { pair[0][0] = sg; pair[0][1] = -1; pair[1][0] = sg; pair[1][1] = 1; }
+    else { pair[0][0] = -1; pair[0][1] = sg; pair[1][0] = 1; pair[1][1] = sg; }
+    for (int k = 0; k < 2; k++) {
+        double v;
+        if (score(s, pair[k][0], pair[k][1], 1, KIND_SDSP, &v) &&
+            (v < bs || (v == bs && bx == mx && by == my))) {
+            bx = pair[k][0]; by = pair[k][1]; bs = v;
+        }
+    }
+    if (abs(mx) + abs(my) == 1 && bx == mx && by == my) { *mvx = bx; *mvy = by; *best = bs; return; }
+    ds_from(s, 2, &bx, &by, &bs);
+    *mvx = bx; *mvy = by; *best = bs;
+}
+
+/* HEXBS (ref. [12]; reading C25): the large hexagon at the origin (7 points), repeated
+ * on the BMP until the BMP is its centre, then the 4 distance-1 points once.  hex = HEXH for
+ * h-HEXBS (Fig. 2a), HEXV for v-HEXBS (Fig. 2b). */
+static void hexbs_search(search_t* s, const int (*hex)[2], int* mvx, int* mvy, double* best) {
+    double s0;
+    score(s, 0, 0, 0, KIND_HEX, &s0);
+    int bx = 0, by = 0, cx = 0, cy = 0, step = 0;
+    double bs = s0;
+    for (;;) {
+        scan(s, cx, cy, hex, 6, step++, KIND_HEX, &bx, &by, &bs);
+        if (bx == cx && by == cy) break;
+        cx = bx; cy = by;
+    }
+    scan(s, cx, cy, SDSP, 4, step, KIND_SDSP, &bx, &by, &bs);
+    *mvx = bx; *mvy = by; *best = bs;
+}
+
+/* Algorithm ids (oracle.h): 0 DCDS, 1 DCDS^S, 2 CDS, 3 DS, 4 h-HEXBS, 5 v-HEXBS. */
+static void run_search(search_t* s, int alg, int* mvx, int* mvy, double* best) {
+    memset(s->seen, 0, (size_t)s->side * s->side);
+    s->points = 0;
+    s->trace_len = 0;
+    switch (alg) {
+        case 0: case 1: dcds_search(s, alg, mvx, mvy, best); break;
+        case 2: cds_search(s, mvx, mvy, best); break;
+        case 3: ds_search(s, mvx, mvy, best); break;
+        case 4: hexbs_search(s, HEXH, mvx, mvy, best); break;
+        default: hexbs_search(s, HEXV, mvx, mvy, best); break;
+    }
+}
+
+static int alg_ok(int alg) { return alg >= 0 && alg <= 5; }
+
 static int search_init(search_t* s, int p) {
     s->p = p;
     s->side = 2 * p + 1;
@@ -235,14 +340,14 @@ int oracle_dcds_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int 
                       int variant, int bx, int by, int16_t* mv_out, uint32_t* sad_out,
                       uint16_t* points_out) {
     if (check_frame(W, H, B) || p < 1 || !cur || !ref) return -1;
-    if (variant != 0 && variant != 1) return -1;
+    if (!alg_ok(variant)) return -1;
     if (bx < 0 || by < 0 || bx + B > W || by + B > H) return -1;
     search_t s;
     if (search_init(&s, p)) return -1;
     pix_ctx c = {cur, ref, W, H, B, bx, by};
     s.cost = pix_cost; s.ctx = &c;
     int mx, my; double best;
-    dcds_search(&s, variant, &mx, &my, &best);
+    run_search(&s, variant, &mx, &my, &best);
     if (mv_out) { mv_out[0] = (int16_t)mx; mv_out[1] = (int16_t)my; }
     if (sad_out) sad_out[0] = (uint32_t)best;
     if (points_out) points_out[0] = (uint16_t)s.points;
@@ -265,13 +370,13 @@ int oracle_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int
 int oracle_dcds_cost(oracle_cost_fn cost, void* ctx, int p, int variant,
                      int* mv_dx, int* mv_dy, double* cost_out, int* points_out,
                      int* trace, int trace_cap, int* trace_len) {
-    if (!cost || p < 1 || (variant != 0 && variant != 1)) return -1;
+    if (!cost || p < 1 || !alg_ok(variant)) return -1;
     search_t s;
     if (search_init(&s, p)) return -1;
     s.cost = cost; s.ctx = ctx;
     s.trace = trace; s.trace_cap = trace ? trace_cap : 0;
     int mx, my; double best;
-    dcds_search(&s, variant, &mx, &my, &best);
+    run_search(&s, variant, &mx, &my, &best);
     if (mv_dx) *mv_dx = mx;
     if (mv_dy) *mv_dy = my;
     if (cost_out) *cost_out = best;
@@ -290,7 +395,7 @@ static double ideal_cost(int dx, int dy, void* ctx) {
 }
 
 int oracle_ideal_nsp_map(int p, int variant, int* nsp_out, int* mvx_out, int* mvy_out) {
-    if (p < 1 || !nsp_out) return -1;
+    if (p < 1 || !nsp_out || !alg_ok(variant)) return -1;
     int side = 2 * p + 1;
     for (int ty = -p; ty <= p; ty++) {
         for (int tx = -p; tx <= p; tx++) {

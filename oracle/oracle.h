@@ -40,7 +40,9 @@ int oracle_sse_block(const uint8_t* cur, const uint8_t* ref, int W, int H, int B
 
 /* DCDS over every block of one frame pair (Steps 1-4).
  * variant 0 = DCDS; variant 1 = DCDS^S (Step 4 checks only the middle point on the
- * side of the cheaper distant point; reading C22).
+ * side of the cheaper distant point; reading C22).  The comparison BMAs of the paper run on
+ * the same machinery (readings C23-C26): variant 2 = CDS (ref. [13]),
+ * 3 = DS (ref. [10]), 4 = h-HEXBS (ref. [12], Fig. 2a), 5 = v-HEXBS (Fig. 2b).
  * mv_out[2*i] = dx, mv_out[2*i+1] = dy; sad_out[i]; points_out[i] = NSP of block i. */
 int oracle_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int B, int p,
                 int variant, int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out);
@@ -64,11 +66,13 @@ int oracle_fullsearch_block(const uint8_t* cur, const uint8_t* ref, int W, int H
 int oracle_mc_psnr(const uint8_t* cur, const uint8_t* ref, int W, int H, int B,
                    const int16_t* mv, double* psnr_out, uint64_t* sse_out);
 
-/* DCDS on an injected cost function (the ideal unimodal surface).  cost(dx,dy,ctx)
+/* DCDS (or, by variant, a comparison BMA) on an injected cost function (the ideal
+ * unimodal surface).  cost(dx,dy,ctx)
  * is called once per distinct feasible candidate.  trace (may be NULL) receives up to
  * trace_cap records of 4 ints {pass, dx, dy, kind}: pass 0 is Step 1 (HCSP), passes
  * 1..n the intermediate steps (1 = Step 2, 2..n = Step 3 repetitions) and pass n+1 Step 4;
- * kind 0=HCSP 1=HDSP 2=VDSP 3=middle point.  *trace_len receives the number of records written. */
+ * kind 0=HCSP 1=HDSP 2=VDSP 3=middle point 4=large diamond 5=small diamond 6=5x5 cross
+ * 7=hexagon.  *trace_len receives the number of records written. */
 typedef double (*oracle_cost_fn)(int dx, int dy, void* ctx);
 int oracle_dcds_cost(oracle_cost_fn cost, void* ctx, int p, int variant,
                      int* mv_dx, int* mv_dy, double* cost_out, int* points_out,
