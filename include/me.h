@@ -95,6 +95,35 @@ int me_dcds_s_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_strid
                     int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
                     uint16_t* points_out, uint64_t* stats_out);
 
+/* Block-matching algorithm ids of me_bma_batch.  DCDS / DCDS^S are the paper's method; the
+ * others are the comparison BMAs the paper measures DCDS against (Table VII
+ * P:307-324), with the readings of DESIGN.md C23-C26:
+ *   CDS     (ref. [13]) 9-point 5x5 cross, first-step stop; the two unchecked central-3x3
+ *           points beside the arm of the BMP (a tie moves the BMP there), second-step stop for
+ *           a distance-1 BMP; then DS from the BMP.
+ *   DS      (ref. [10]) large diamond (9 points, then 8 recentred) until the BMP is its centre,
+ *           then the small diamond (4 points).
+ *   HEXBS_H (ref. [12], Fig. 2a) horizontal hexagon {(+-2,0),(+-1,+-2)} until centred, then the
+ *           4 distance-1 points; HEXBS_V the vertical hexagon (Fig. 2b).
+ * All share the conventions above: visited set (each position scored once per block), strict
+ * compare, window-only feasibility, edge-replicated reference; points of a pattern are
+ * scanned in ascending distance from its centre, ties by (|dy|,|dx|,dy,dx). */
+typedef enum {
+    ME_ALG_DCDS = 0,
+    ME_ALG_DCDS_S = 1,
+    ME_ALG_CDS = 2,
+    ME_ALG_DS = 3,
+    ME_ALG_HEXBS_H = 4,
+    ME_ALG_HEXBS_V = 5
+} me_alg;
+
+/* Any me_alg over npairs pairs; arguments, layout, outputs (mv, SAD, NSP, stats = {sum points,
+ * sum SAD, SSE at the chosen MVs}) and errors exactly as me_dcds_batch (ME_EINVAL for an
+ * unknown alg).  ME_ALG_DCDS / ME_ALG_DCDS_S run the me_dcds_batch / me_dcds_s_batch kernels. */
+int me_bma_batch(int alg, const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride,
+                 int npairs, int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
+                 uint16_t* points_out, uint64_t* stats_out);
+
 /* Full search over npairs pairs; same layout as me_dcds_batch (stats: {sum points, sum SAD,
  * SSE at the FS MVs}). */
 int me_fullsearch_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride,

@@ -15,6 +15,7 @@
 #include <cmath>
 
 #include "../../include/me.h"
+#include "bma_kernel.cuh"
 #include "dcds_kernel.cuh"
 #include "fs_kernel.cuh"
 
@@ -214,6 +215,61 @@ int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npa
     return ME_OK;
 }
 
+// The comparison BMAs on the DCDS engine's default geometry.
+template <int B, int G, int NW>
+void launch_bma_b(int alg, dim3 grid, size_t smem, const CUtensorMap& tc, const CUtensorMap& tr,
+                  const me::BmaArgs& a, cudaStream_t s) {
+    switch (alg) {
+        case me::ALG_CDS: me::bma_kernel<B, G, NW, me::ALG_CDS><<<grid, NW * 32, smem, s>>>(tc, tr, a); break;
+        case me::ALG_DS: me::bma_kernel<B, G, NW, me::ALG_DS><<<grid, NW * 32, smem, s>>>(tc, tr, a); break;
+        case me::ALG_HEXBS_H: me::bma_kernel<B, G, NW, me::ALG_HEXBS_H><<<grid, NW * 32, smem, s>>>(tc, tr, a); break;
+        default: me::bma_kernel<B, G, NW, me::ALG_HEXBS_V><<<grid, NW * 32, smem, s>>>(tc, tr, a); break;
+    }
+}
+
+int run_bma(int alg, const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W,
+            int H, int block, int p, int16_t* mv, uint32_t* sad, uint16_t* pts, uint64_t* stats,
+            cudaStream_t s) {
+    // geometry of the DCDS defaults (B=8: G=2, 4 warps, 16x4 tiles; B=16: G=8, 8 warps, 8x4)
+    const int B = block, nbx = W / B, nby = H / B;
+    const int G = B == 16 ? 8 : 2, NW = B == 16 ? 8 : 4;
+    int tbx = std::min(B == 16 ? 8 : 16, nbx), tby = std::min(4, nby);
+    while ((tbx * B) % 16) tbx++;
+    me::BmaArgs a;
+    a.cur0 = cur0; a.ref0 = ref0; a.stride = stride;
+    a.W = W; a.H = H; a.p = p;
+    a.tbx = tbx; a.tby = tby;
+    a.ntx = (nbx + tbx - 1) / tbx;
+    const int nty = (nby + tby - 1) / tby;
+    const int TW = tbx * B, TH = tby * B;
+    int pitch = ((TW + 2 * p + 31) + 15) & ~15;
+    if (((pitch >> 4) & 1) == 0) pitch += 16;
+    a.pitch = pitch;
+    a.rh = TH + 2 * p;
+    const int side = 2 * p + 1;
+    a.bm_words = (((side * side + 31) / 32) + 3) & ~3;
+    a.nbx = nbx; a.nb = nbx * nby;
+    a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;
+    a.mv = reinterpret_cast<uint32_t*>(mv); a.sad = sad; a.pts = pts;
+    a.stats = reinterpret_cast<unsigned long long*>(stats);
+    for (int r = 0; r < me::NROW; r++) a.rcode[r] = me::row_code(r);
+    const int groups = NW * 32 / G;
+    const size_t smem = 128 + (size_t)a.cur_off + (size_t)TW * TH + (size_t)groups * a.bm_words * 4 + 32;
+    if ((int)smem > g_smem_optin) return fail(ME_EINVAL, "tile does not fit in shared memory");
+    CUtensorMap tc, tr;
+    int rc = make_tmap(&tc, cur0, W, H, npairs, stride, TW, TH);
+    if (rc) return rc;
+    rc = make_tmap(&tr, ref0, W, H, npairs, stride, a.pitch, a.rh);
+    if (rc) return rc;
+    if (stats) CK(cudaMemsetAsync(stats, 0, sizeof(uint64_t) * 3 * (size_t)npairs, s));
+    const dim3 grid(a.ntx * nty, npairs);
+    if (B == 16) launch_bma_b<16, 8, 8>(alg, grid, smem, tc, tr, a, s);
+    else launch_bma_b<8, 2, 4>(alg, grid, smem, tc, tr, a, s);
+    g_launches++;
+    CK(cudaGetLastError());
+    return ME_OK;
+}
+
 int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W, int H,
            int block, int p, int16_t* mv, uint32_t* sad, uint16_t* pts, uint64_t* stats,
            cudaStream_t s) {
@@ -327,6 +383,14 @@ int me_init(int device) {
     if ((rc = allow_smem(me::dcds_kernel<B, G, 8, V>))) return rc;
     ME_DCDS_KERNELS(ME_ALLOW)
 #undef ME_ALLOW
+#define ME_ALLOW_BMA(B, G, NW)                                                           \
+    if ((rc = allow_smem(me::bma_kernel<B, G, NW, me::ALG_CDS>))) return rc;            \
+    if ((rc = allow_smem(me::bma_kernel<B, G, NW, me::ALG_DS>))) return rc;             \
+    if ((rc = allow_smem(me::bma_kernel<B, G, NW, me::ALG_HEXBS_H>))) return rc;        \
+    if ((rc = allow_smem(me::bma_kernel<B, G, NW, me::ALG_HEXBS_V>))) return rc;
+    ME_ALLOW_BMA(8, 2, 4)
+    ME_ALLOW_BMA(16, 8, 8)
+#undef ME_ALLOW_BMA
     if ((rc = allow_smem(me::fs_kernel<16>))) return rc;
     if ((rc = allow_smem(me::fs_kernel<8>))) return rc;
     if (!g_scratch) CK(cudaMalloc(&g_scratch, 64));
@@ -371,6 +435,22 @@ int me_dcds_s_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_strid
     if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
     return run_dcds(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
                     stats_out, 1, g_stream);
+}
+
+int me_bma_batch(int alg, const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                 int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
+                 uint16_t* points_out, uint64_t* stats_out) {
+    if (alg < ME_ALG_DCDS || alg > ME_ALG_HEXBS_V) return fail(ME_EINVAL, "unknown algorithm id");
+    int rc = validate_search(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out,
+                             points_out);
+    if (rc) return rc;
+    if (stats_out && !aligned(stats_out, 8)) return fail(ME_EALIGN, "stats_out must be 8-byte aligned");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    if (alg <= ME_ALG_DCDS_S)
+        return run_dcds(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
+                        stats_out, alg, g_stream);
+    return run_bma(alg, cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
+                   stats_out, g_stream);
 }
 
 int me_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int block, int p,

@@ -20,8 +20,11 @@ ME_OK, ME_EINVAL, ME_EALIGN, ME_ENOTINIT, ME_ECUDA, ME_ENOMEM = 0, -1, -2, -3, -
 SYMBOLS = (
     "me_init", "me_set_stream", "me_dcds", "me_fullsearch", "me_mc_psnr", "me_dcds_batch",
     "me_dcds_s_batch", "me_fullsearch_batch", "me_mc_sse_batch", "me_dcds_batch_host",
-    "me_launch_count", "me_strerror", "me_shutdown", "me_quality_batch",
+    "me_launch_count", "me_strerror", "me_shutdown", "me_quality_batch", "me_bma_batch",
 )
+
+# me_alg ids (include/me.h)
+ALGS = {"dcds": 0, "dcds_s": 1, "cds": 2, "ds": 3, "hexbs_h": 4, "hexbs_v": 5}
 
 
 class MEError(RuntimeError):
@@ -56,6 +59,7 @@ def load() -> ctypes.CDLL:
     L.me_dcds_batch_host.argtypes = batch
     L.me_mc_sse_batch.argtypes = [vp, vp, i64, i32, i32, i32, i32, vp, vp]
     L.me_quality_batch.argtypes = [vp, vp, i32, i32, vp]
+    L.me_bma_batch.argtypes = [i32] + batch
     L.me_launch_count.argtypes = []
     L.me_launch_count.restype = i64
     L.me_strerror.argtypes = [i32]
@@ -154,6 +158,13 @@ def me_dcds_s_batch(frames, block, p, mv, sad, pts, stats=None):
 
 def me_fullsearch_batch(frames, block, p, mv, sad, pts, stats=None):
     _batch(load().me_fullsearch_batch, frames, block, p, mv, sad, pts, stats)
+
+
+def me_bma_batch(alg, frames, block, p, mv, sad, pts, stats=None):
+    """Any block-matching algorithm of :data:`ALGS` (name or id) over a batch of pairs."""
+    a = ALGS[alg] if isinstance(alg, str) else int(alg)
+    fn = load().me_bma_batch
+    _batch(lambda *args: fn(a, *args), frames, block, p, mv, sad, pts, stats)
 
 
 def me_dcds_batch_host(frames, block, p, mv, sad, pts, stats=None):

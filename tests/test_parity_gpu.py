@@ -39,8 +39,11 @@ def gpu_search(frames, B, p, kind="dcds"):
     n, _, H, W = frames.shape
     nb = (W // B) * (H // B)
     mv, sad, pts, st = me.alloc_outputs(n, nb, frames.device)
-    fn = {"dcds": me.me_dcds_batch, "dcds_s": me.me_dcds_s_batch, "fs": me.me_fullsearch_batch}[kind]
-    fn(frames, B, p, mv, sad, pts, st)
+    fn = {"dcds": me.me_dcds_batch, "dcds_s": me.me_dcds_s_batch, "fs": me.me_fullsearch_batch}.get(kind)
+    if fn is None:  # a comparison BMA
+        me.me_bma_batch(kind, frames, B, p, mv, sad, pts, st)
+    else:
+        fn(frames, B, p, mv, sad, pts, st)
     torch.cuda.synchronize()
     return (to_np(mv), to_np(sad).astype(np.uint32), to_np(pts).astype(np.uint16),
             to_np(st).astype(np.uint64))
@@ -51,7 +54,7 @@ def assert_pair_equal(host_pair, B, p, mv, sad, pts, kind="dcds", tag=""):
     if kind == "fs":
         omv, osad, opts = oracle.fullsearch(cur, ref, B, p)
     else:
-        omv, osad, opts = oracle.dcds(cur, ref, B, p, 1 if kind == "dcds_s" else 0)
+        omv, osad, opts = oracle.bma(cur, ref, B, p, kind)
     bad = np.flatnonzero((mv != omv).any(1) | (sad != osad) | (pts != opts))
     assert bad.size == 0, (f"{tag} {kind} B={B} p={p}: {bad.size} blocks differ, first {bad[:5]}: "
                            f"gpu {mv[bad[0]]},{sad[bad[0]]},{pts[bad[0]]} "
@@ -329,3 +332,71 @@ def test_quality_kernel_examples_and_parity():
     rep = report.compare_dcds_fs(fr, cfg.B, cfg.p)
     assert rep["FS"]["prob"] == 1.0 and rep["FS"]["dist"] == 0.0 and rep["FS"]["nsp"] == 225.0
     assert rep["FS"]["mad"] <= rep["DCDS"]["mad"] and rep["DCDS"]["nsp"] < 225.0
+
+
+# ---------------------------------------------------------------------------------------
+# Comparison BMAs: CDS, DS, h-/v-HEXBS through me_bma_batch.
+# ---------------------------------------------------------------------------------------
+BMAS = ["cds", "ds", "hexbs_h", "hexbs_v"]
+
+
+@pytest.mark.parametrize("alg", BMAS)
+def test_bma_c0_c1_c2(alg):
+    for name, pairs in (("c0", None), ("c1", range(0, 29, 4)), ("c2", range(1, 300, 37))):
+        cfg = synth.CONFIGS[name]
+        fr = synth.make_sequence(cfg, device=DEV, pairs=pairs)
+        host = to_np(fr)
+        mv, sad, pts, st = gpu_search(fr, cfg.B, cfg.p, alg)
+        for t in range(fr.shape[0]):
+            omv, osad, opts = assert_pair_equal(host[t], cfg.B, cfg.p, mv[t], sad[t], pts[t], alg,
+                                                tag=f"{name}/{t}")
+            _, osse = oracle.mc_psnr(host[t, 0], host[t, 1], cfg.B, omv)
+            assert st[t].tolist() == [int(opts.astype(np.int64).sum()), int(osad.astype(np.int64).sum()), osse]
+
+
+@pytest.mark.parametrize("alg", BMAS)
+@pytest.mark.parametrize("kind,W,H", [("flat", 176, 144), ("binary", 176, 144), ("random", 176, 144),
+                                      ("border16", 48, 48), ("tiny", 16, 16), ("wide", 400, 32)])
+@pytest.mark.parametrize("B", [16, 8])
+@pytest.mark.parametrize("p", [1, 2, 7, 32])
+def test_bma_special_inputs(alg, kind, W, H, B, p):
+    if W % B or H % B:
+        pytest.skip("frame not divisible by block")
+    cur, ref = special_pair(kind, W, H, seed=p * 5 + B)
+    mv, sad, pts, _ = gpu_search(frames_from_np(cur, ref), B, p, alg)
+    assert_pair_equal(np.stack([cur, ref]), B, p, mv[0], sad[0], pts[0], alg, tag=kind)
+
+
+@pytest.mark.parametrize("B", [16, 8])
+@pytest.mark.parametrize("alg,fixture", [("cds", "table7_cds.txt"), ("ds", "table7_ds.txt")])
+def test_bma_ideal_mosaic_table7(B, alg, fixture):
+    """The kernels reproduce Table VII's CDS and DS blocks through pixels."""
+    cur, ref, tile, off, blocks = synth.ideal_mosaic(B, 7)
+    mv, sad, pts, _ = gpu_search(frames_from_np(cur, ref), B, 7, alg)
+    np.testing.assert_array_equal(pts[0][blocks][7:, 7:], golden_matrix(fixture, int))
+    assert_pair_equal(np.stack([cur, ref]), B, 7, mv[0], sad[0], pts[0], alg, tag="mosaic")
+
+
+@pytest.mark.parametrize("alg", BMAS)
+def test_bma_c3_c4_sampled(alg):
+    """Full-size frames, bench launch configuration (all pairs of a chunk in one launch),
+    checked on sampled blocks computed one by one by the oracle."""
+    rng = np.random.default_rng(17)
+    for name, pairs in (("c3", [0, 57, 123]), ("c4", [0, 311])):
+        cfg = synth.CONFIGS[name]
+        fr = synth.make_sequence(cfg, device=DEV, pairs=pairs)
+        host = to_np(fr)
+        mv, sad, pts, _ = gpu_search(fr, cfg.B, cfg.p, alg)
+        nbx = cfg.W // cfg.B
+        for t in range(len(pairs)):
+            for i in rng.choice(cfg.nb, 150, replace=False):
+                bx, by = (i % nbx) * cfg.B, (i // nbx) * cfg.B
+                omv, osad, opts = oracle.bma_block(host[t, 0], host[t, 1], cfg.B, cfg.p, bx, by, alg)
+                assert (tuple(mv[t, i]), sad[t, i], pts[t, i]) == (omv, osad, opts), (name, t, i)
+
+
+def test_bma_unknown_alg_rejected():
+    fr = synth.make_sequence(synth.CONFIGS["c0"], device=DEV)
+    mv, sad, pts, st = me.alloc_outputs(1, 99, DEV)
+    with pytest.raises(me.MEError):
+        me.me_bma_batch(6, fr, 16, 7, mv, sad, pts, st)
