@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-fs", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cmp", action="store_true", help="skip the comparison-BMA section")
     ap.add_argument("--e2e-steps", type=int, default=5)
     return ap.parse_args()
 
@@ -374,6 +375,16 @@ def main():
         if r_clk is not None:
             fsline["alu_frac"] = (fs_ops / fs_s) / roofline["int_peak_lane_ops_per_s"]
         line["fullsearch"] = fsline
+
+    if rank == 0 and not args.no_cmp:
+        # the paper's comparison (Table IX): every BMA on a
+        # sample of the same pairs -- NSP, PSNR, distance / probability vs FS, NSP speed-up of
+        # DCDS over each (the "up to 54.9%" measure, P:9), and its own kernel throughput
+        from paper_0806_0689_b200 import report
+        ncmp = min(n, 16)
+        rows = report.compare_bmas(frames[:ncmp], cfg.B, cfg.p, reps=3)
+        line["comparison"] = {"pairs": ncmp, "algs": {
+            a: {k: (round(v, 6) if isinstance(v, float) else v) for k, v in r.items()} for a, r in rows.items()}}
 
     if rank == 0 and not args.no_e2e:
         # end to end through the C ABI on HOST buffers: H2D of the frames (pinned), search,

@@ -54,3 +54,43 @@ def compare_dcds_fs(frames: torch.Tensor, B: int, p: int):
     torch.cuda.synchronize()
     return {"DCDS": sequence_means(pair_rows(d[3], q, W, H, B)),
             "FS": sequence_means(pair_rows(f[3], qfs, W, H, B))}
+
+
+# The paper's Table IX compares DCDS with the other BMAs on the same sequences;
+# ALGS of the comparison (me.ALGS names) in the order the report prints them.
+TABLE9_ALGS = ("dcds", "dcds_s", "cds", "ds", "hexbs_h", "hexbs_v")
+
+
+def compare_bmas(frames: torch.Tensor, B: int, p: int, algs=TABLE9_ALGS, fs: bool = True, reps: int = 0):
+    """Table-IX-style rows (MAD, MSE, NSP, PSNR, distance and hit probability against FS) of
+    every algorithm on device frames [n, 2, H, W], plus the NSP speed-up of DCDS over each
+    (NSP_alg / NSP_DCDS - 1, the paper's "up to 54.9%" measure, P:9).  With reps > 0
+    each search is also timed (CUDA events, mean of reps launches) -> "blocks_per_s"."""
+    n, _, H, W = frames.shape
+    nb = (W // B) * (H // B)
+    f = me.alloc_outputs(n, nb, frames.device)
+    me.me_fullsearch_batch(frames, B, p, *f)
+    out = {}
+    for alg in algs:
+        d = me.alloc_outputs(n, nb, frames.device)
+        me.me_bma_batch(alg, frames, B, p, *d)
+        q = me.me_quality_batch(d[0], f[0])
+        torch.cuda.synchronize()
+        row = sequence_means(pair_rows(d[3], q, W, H, B))
+        if reps:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                me.me_bma_batch(alg, frames, B, p, *d)
+            b.record()
+            torch.cuda.synchronize()
+            row["blocks_per_s"] = n * nb * reps / (a.elapsed_time(b) * 1e-3)
+        out[alg] = row
+    if fs:
+        torch.cuda.synchronize()
+        out["fs"] = sequence_means(pair_rows(f[3], me.me_quality_batch(f[0], f[0]), W, H, B))
+    if "dcds" in out:
+        base = out["dcds"]["nsp"]
+        for alg, row in out.items():
+            row["nsp_speedup_of_dcds"] = row["nsp"] / base - 1.0
+    return out
