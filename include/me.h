@@ -124,6 +124,21 @@ int me_bma_batch(int alg, const uint8_t* cur0, const uint8_t* ref0, int64_t pair
                  int npairs, int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
                  uint16_t* points_out, uint64_t* stats_out);
 
+/* The ideal condition of P:299-301 (Table VII): for every true MV t of the +-p
+ * window, run algorithm `alg` on the unimodal surface whose distortion at candidate q is the
+ * Euclidean distance |q - t| (the device uses |q - t|^2, which orders and ties candidates
+ * identically), with the same readings as the pixel searches.  Outputs (DEVICE int32 arrays
+ * of (2p+1)^2, row-major over (ty, tx), i.e. index (ty+p)*(2p+1) + tx+p): nsp_out = number of
+ * search points; mvx_out / mvy_out (may be NULL) = the MV found.  1 <= p <= 32. */
+int me_ideal_nsp_map(int alg, int p, int32_t* nsp_out, int32_t* mvx_out, int32_t* mvy_out);
+
+/* MV histogram (the MVP distribution of P:71-98): hist_out[(dy+p)*(2p+1) + dx+p] = number of
+ * the n vectors mv[i] = (dx,dy) (DEVICE int16 pairs) inside the +-p window (others are not
+ * counted; mv may be NULL when n == 0).  hist_out: DEVICE uint64 [(2p+1)^2], overwritten.
+ * 1 <= p <= 32.  Table II / III /
+ * Fig. 3 statistics are host arithmetic on this histogram (paper_0806_0689_b200/mvstats.py). */
+int me_mv_hist(const int16_t* mv, int64_t n, int p, uint64_t* hist_out);
+
 /* Full search over npairs pairs; same layout as me_dcds_batch (stats: {sum points, sum SAD,
  * SSE at the FS MVs}). */
 int me_fullsearch_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride,

@@ -16,6 +16,7 @@
 
 #include "../../include/me.h"
 #include "bma_kernel.cuh"
+#include "ideal_kernel.cuh"
 #include "dcds_kernel.cuh"
 #include "fs_kernel.cuh"
 
@@ -451,6 +452,41 @@ int me_bma_batch(int alg, const uint8_t* cur0, const uint8_t* ref0, int64_t pair
                         stats_out, alg, g_stream);
     return run_bma(alg, cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
                    stats_out, g_stream);
+}
+
+int me_ideal_nsp_map(int alg, int p, int32_t* nsp_out, int32_t* mvx_out, int32_t* mvy_out) {
+    if (alg < ME_ALG_DCDS || alg > ME_ALG_HEXBS_V) return fail(ME_EINVAL, "unknown algorithm id");
+    if (p < 1 || p > 32) return fail(ME_EINVAL, "p must be in [1, 32]");
+    if (!nsp_out) return fail(ME_EINVAL, "NULL nsp_out");
+    if (!aligned(nsp_out, 4) || (mvx_out && !aligned(mvx_out, 4)) || (mvy_out && !aligned(mvy_out, 4)))
+        return fail(ME_EALIGN, "int32 outputs must be 4-byte aligned");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    me::IdealArgs a;
+    a.alg = alg; a.p = p; a.nsp = nsp_out; a.mvx = mvx_out; a.mvy = mvy_out;
+    for (int r = 0; r < me::NROW_ALL; r++) a.rcode[r] = me::any_row_code(r);
+    const int n = (2 * p + 1) * (2 * p + 1);
+    me::ideal_kernel<<<(n + 127) / 128, 128, 0, g_stream>>>(a);
+    g_launches++;
+    CK(cudaGetLastError());
+    return ME_OK;
+}
+
+int me_mv_hist(const int16_t* mv, int64_t n, int p, uint64_t* hist_out) {
+    if ((!mv && n > 0) || !hist_out) return fail(ME_EINVAL, "NULL pointer");
+    if (n < 0 || p < 1 || p > 32) return fail(ME_EINVAL, "bad n / p");
+    if (!aligned(mv, 4) || !aligned(hist_out, 8)) return fail(ME_EALIGN, "misaligned pointer");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    const int nbin = (2 * p + 1) * (2 * p + 1);
+    CK(cudaMemsetAsync(hist_out, 0, sizeof(uint64_t) * nbin, g_stream));
+    if (n > 0) {
+        const long long want = (n + 255) / 256;
+        const int grid = (int)std::min<long long>(want, 4 * 148);
+        me::mv_hist_kernel<<<grid, 256, nbin * sizeof(unsigned int), g_stream>>>(
+            reinterpret_cast<const uint32_t*>(mv), n, p, reinterpret_cast<unsigned long long*>(hist_out));
+        g_launches++;
+    }
+    CK(cudaGetLastError());
+    return ME_OK;
 }
 
 int me_dcds(const uint8_t* cur, const uint8_t* ref, int W, int H, int block, int p,

@@ -21,6 +21,7 @@ SYMBOLS = (
     "me_init", "me_set_stream", "me_dcds", "me_fullsearch", "me_mc_psnr", "me_dcds_batch",
     "me_dcds_s_batch", "me_fullsearch_batch", "me_mc_sse_batch", "me_dcds_batch_host",
     "me_launch_count", "me_strerror", "me_shutdown", "me_quality_batch", "me_bma_batch",
+    "me_ideal_nsp_map", "me_mv_hist",
 )
 
 # me_alg ids (include/me.h)
@@ -60,6 +61,8 @@ def load() -> ctypes.CDLL:
     L.me_mc_sse_batch.argtypes = [vp, vp, i64, i32, i32, i32, i32, vp, vp]
     L.me_quality_batch.argtypes = [vp, vp, i32, i32, vp]
     L.me_bma_batch.argtypes = [i32] + batch
+    L.me_ideal_nsp_map.argtypes = [i32, i32, vp, vp, vp]
+    L.me_mv_hist.argtypes = [vp, i64, i32, vp]
     L.me_launch_count.argtypes = []
     L.me_launch_count.restype = i64
     L.me_strerror.argtypes = [i32]
@@ -165,6 +168,26 @@ def me_bma_batch(alg, frames, block, p, mv, sad, pts, stats=None):
     a = ALGS[alg] if isinstance(alg, str) else int(alg)
     fn = load().me_bma_batch
     _batch(lambda *args: fn(a, *args), frames, block, p, mv, sad, pts, stats)
+
+
+def me_ideal_nsp_map(alg, p, device="cuda"):
+    """Ideal-condition NSP map (Table VII) of an algorithm for every true MV of the
+    +-p window: (nsp, mvx, mvy) int32 device tensors of shape [2p+1, 2p+1] indexed [ty+p, tx+p]."""
+    a = ALGS[alg] if isinstance(alg, str) else int(alg)
+    side = 2 * p + 1
+    out = [torch.empty(side, side, dtype=torch.int32, device=device) for _ in range(3)]
+    _check(load().me_ideal_nsp_map(a, p, *(_ptr(t) for t in out)))
+    return tuple(out)
+
+
+def me_mv_hist(mv, p, hist=None):
+    """Histogram [2p+1, 2p+1] (uint64 as int64) of an int16 MV field [..., 2] on the device."""
+    side = 2 * p + 1
+    if hist is None:
+        hist = torch.empty(side, side, dtype=torch.int64, device=mv.device)
+    n = mv.numel() // 2
+    _check(load().me_mv_hist(_ptr(mv), n, p, _ptr(hist)))
+    return hist
 
 
 def me_dcds_batch_host(frames, block, p, mv, sad, pts, stats=None):

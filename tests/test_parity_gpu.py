@@ -400,3 +400,62 @@ def test_bma_unknown_alg_rejected():
     mv, sad, pts, st = me.alloc_outputs(1, 99, DEV)
     with pytest.raises(me.MEError):
         me.me_bma_batch(6, fr, 16, 7, mv, sad, pts, st)
+
+
+# ---------------------------------------------------------------------------------------
+# ideal-condition simulator and MV histogram on the GPU.
+# ---------------------------------------------------------------------------------------
+ALL_ALGS = ["dcds", "dcds_s", "cds", "ds", "hexbs_h", "hexbs_v"]
+
+
+@pytest.mark.parametrize("alg", ALL_ALGS)
+@pytest.mark.parametrize("p", [1, 2, 7, 15, 16, 32])
+def test_ideal_map_matches_oracle(alg, p):
+    nsp, mx, my = (to_np(t) for t in me.me_ideal_nsp_map(alg, p))
+    onsp, omx, omy = oracle.ideal_nsp_map(p, oracle.ALGS[alg])
+    np.testing.assert_array_equal(nsp, onsp)
+    np.testing.assert_array_equal(mx, omx)
+    np.testing.assert_array_equal(my, omy)
+
+
+@pytest.mark.parametrize("alg,fixture", [("dcds", "table7_dcds.txt"), ("cds", "table7_cds.txt"),
+                                         ("ds", "table7_ds.txt")])
+def test_ideal_map_table7_and_table8(alg, fixture):
+    """Table VII out of the GPU simulator, and Table VIII distribution 2."""
+    from paper_0806_0689_b200 import mvstats
+    nsp = to_np(me.me_ideal_nsp_map(alg, 7)[0])
+    np.testing.assert_array_equal(nsp[7:, 7:], golden_matrix(fixture, int))
+    printed = {"dcds": 9.7, "cds": 12.5, "ds": 14.8}[alg]
+    assert abs(mvstats.ansp(nsp, golden_matrix("table2_mvp.txt", float)) - printed) <= 0.05 + 1e-9
+
+
+def test_mv_hist_matches_numpy():
+    rng = np.random.default_rng(3)
+    for n, p in [(0, 7), (1, 1), (12345, 7), (1 << 20, 32)]:
+        mv = rng.integers(-p - 2, p + 3, size=(n, 2)).astype(np.int16)
+        h = to_np(me.me_mv_hist(torch.from_numpy(mv).to(DEV), p))
+        side = 2 * p + 1
+        ok = (np.abs(mv) <= p).all(axis=1)
+        ref = np.bincount(((mv[ok, 1] + p) * side + mv[ok, 0] + p).astype(np.int64),
+                          minlength=side * side).reshape(side, side)
+        np.testing.assert_array_equal(h, ref)
+
+
+def test_mvp_statistics_of_fs_fields():
+    """Table II/III-style statistics of the FS motion fields of c1 (the paper computes them on
+    FS fields): GPU FS + GPU histogram equal the oracle's FS fields counted in numpy."""
+    from paper_0806_0689_b200 import mvstats
+    cfg = synth.CONFIGS["c1"]
+    fr = synth.make_sequence(cfg, device=DEV, pairs=range(1, 6))
+    mv, sad, pts, st = gpu_search(fr, cfg.B, cfg.p, "fs")
+    h = to_np(me.me_mv_hist(torch.from_numpy(mv).to(DEV), cfg.p)).astype(np.float64)
+    host = to_np(fr)
+    ref = np.zeros_like(h)
+    for t in range(host.shape[0]):
+        omv, _, _ = oracle.fullsearch(host[t, 0], host[t, 1], cfg.B, cfg.p)
+        for dx, dy in omv:
+            ref[dy + cfg.p, dx + cfg.p] += 1
+    np.testing.assert_array_equal(h, ref)
+    P = mvstats.normalise(h)
+    hs, vs = mvstats.axis_shares(mvstats.quarter(P))
+    assert 0 < vs < hs < 1  # the synthetic mix is horizontally biased (2:1, BASELINE configs)
