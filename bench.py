@@ -248,28 +248,47 @@ def main():
     n = cfg.npairs
     pairs = range(1 + rank * n, 1 + (rank + 1) * n)
     frames = synth.make_sequence(cfg, device=dev, pairs=pairs)
-    mv, sad, pts, st = me.alloc_outputs(n, cfg.nb, dev)
     in_bytes = frames.numel()
+    from paper_0806_0689_b200 import dist as mdist
+    # outputs: one flat buffer [mv | sad | points | stats] per step in flight; with N > 1 two
+    # of them, so step k+1 searches while step k's buffer is gathered (NCCL, comm stream)
+    nbuf = 2 if ws > 1 else 1
+    flats = [mdist.alloc_flat(n, cfg.nb, dev) for _ in range(nbuf)]
+    views = [mdist.flat_views(f, n, cfg.nb) for f in flats]
+    outs = [mdist.alloc_flat(n, cfg.nb, dev, ws) for _ in range(nbuf)] if ws > 1 else None
+    comm = torch.cuda.Stream(dev) if ws > 1 else None
+    ready = [torch.cuda.Event() for _ in range(nbuf)]
+    freed = [torch.cuda.Event() for _ in range(nbuf)]
+    used = [False] * nbuf
     torch.cuda.synchronize()
 
-    if ws > 1:
-        from paper_0806_0689_b200 import dist as mdist
+    def claim(k):
+        b = k % nbuf
+        if used[b]:
+            stream.wait_event(freed[b])  # the gather of this buffer's previous step is done
+        return b
 
-    def gather():
-        # NCCL all_gather of every rank's per-pair MV field + statistics (one packed record
-        # per pair; paper_0806_0689_b200/dist.py) -- the path's only collective
+    def search(b):
+        me.me_dcds_batch(frames, cfg.B, cfg.p, *views[b])
+        return b
+
+    def gather(b):
+        # NCCL all_gather of every rank's per-pair MV fields + statistics (the flat buffer as
+        # it is; paper_0806_0689_b200/dist.py) -- the path's only collective, overlapped with
+        # the next step's search
         if ws > 1:
-            mdist.gather_fields(mv, sad, pts, st, ws * n)
-
-    def step():
-        me.me_dcds_batch(frames, cfg.B, cfg.p, mv, sad, pts, st)
-        gather()
+            ready[b].record(stream)
+            comm.wait_event(ready[b])
+            with torch.cuda.stream(comm):
+                mdist.gather_flat(flats[b], outs[b])
+            freed[b].record(comm)
+            used[b] = True
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     with ClockSampler(local) as clk:  # started first: warm-up steps also bring clocks up
-        for _ in range(max(args.warmup, 0)):
-            step()
+        for k in range(max(args.warmup, 0)):
+            gather(search(claim(k)))
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
@@ -280,13 +299,20 @@ def main():
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for k in range(args.steps):
+            b = claim(k)  # (a wait on the previous gather is not kernel time)
             ev[k][0].record(stream)
-            me.me_dcds_batch(frames, cfg.B, cfg.p, mv, sad, pts, st)
+            search(b)
             ev[k][1].record(stream)
-            gather()
+            gather(b)
+        if comm is not None:
+            stream.wait_stream(comm)  # the last gathers are inside the timed region
         t_end.record(stream)
         torch.cuda.synchronize()
         clk.mark_end()
+    mv, sad, pts, st = views[(args.steps - 1) % nbuf]
+    if ws > 1:  # the gathered copy of this rank's fields is its own output
+        mine = mdist.unpack_gathered(outs[(args.steps - 1) % nbuf], n, cfg.nb)[rank]
+        assert torch.equal(mine[0], mv) and torch.equal(mine[3], st)
     launches = me.me_launch_count() - launches0
     total_ms = t_start.elapsed_time(t_end)
     kern_ms = [a.elapsed_time(b) for a, b in ev]

@@ -75,3 +75,52 @@ def gather_fields(mv, sad, pts, stats, npairs_total: int, group=None):
     keep = torch.cat([torch.arange(r * per, r * per + (shard(npairs_total, world, r)[1] - shard(npairs_total, world, r)[0]))
                       for r in range(world)])
     return unpack_fields(out[keep.to(out.device)], nb)
+
+
+# ---------------------------------------------------------------------------------------
+# Flat output buffers: the batched search writes its four outputs into ONE device buffer
+# [mv | sad | points | stats], so the gather sends it as-is and the gathered result is unpacked
+# by views -- no packing copies on the step's critical path (bench.py, N > 1).
+# ---------------------------------------------------------------------------------------
+def flat_layout(n: int, nb: int):
+    """Byte offsets and total size of the flat output buffer of n pairs x nb blocks:
+    mv [n, nb, 2] int16 | sad [n, nb] int32 | points [n, nb] int16 | stats [n, 3] int64
+    (stats 8-byte aligned; every part meets the C ABI's alignment)."""
+    o_mv = 0
+    o_sad = o_mv + 4 * n * nb
+    o_pts = o_sad + 4 * n * nb
+    o_st = (o_pts + 2 * n * nb + 7) & ~7
+    total = o_st + 24 * n
+    return o_mv, o_sad, o_pts, o_st, total
+
+
+def flat_views(buf: torch.Tensor, n: int, nb: int):
+    """(mv, sad, points, stats) views of a flat uint8 buffer laid out by flat_layout."""
+    o_mv, o_sad, o_pts, o_st, total = flat_layout(n, nb)
+    assert buf.dtype == torch.uint8 and buf.numel() >= total
+    mv = buf[o_mv:o_sad].view(torch.int16).view(n, nb, 2)
+    sad = buf[o_sad:o_pts].view(torch.int32).view(n, nb)
+    pts = buf[o_pts:o_pts + 2 * n * nb].view(torch.int16).view(n, nb)
+    st = buf[o_st:o_st + 24 * n].view(torch.int64).view(n, 3)
+    return mv, sad, pts, st
+
+
+def alloc_flat(n: int, nb: int, device, world: int = 1):
+    """A flat output buffer, or the [world, size] receive buffer of its gather."""
+    total = flat_layout(n, nb)[4]
+    return torch.empty((world, total) if world > 1 else total, dtype=torch.uint8, device=device)
+
+
+def gather_flat(buf: torch.Tensor, out: torch.Tensor, group=None):
+    """all_gather of every rank's flat buffer into out [world, size] (NCCL: one collective)."""
+    if hasattr(dist, "all_gather_into_tensor") and buf.is_cuda:
+        dist.all_gather_into_tensor(out.view(-1), buf, group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), buf, group=group)
+    return out
+
+
+def unpack_gathered(out: torch.Tensor, n: int, nb: int):
+    """Per-rank (mv, sad, points, stats) views of a gathered [world, size] buffer; rank r's
+    pairs are the global pairs r*n .. r*n+n-1 (weak scaling: every rank searches n pairs)."""
+    return [flat_views(out[r], n, nb) for r in range(out.shape[0])]

@@ -96,3 +96,50 @@ def test_gloo_gather_matches_single_rank(world, npairs):
     ref = [t.numpy() for t in _oracle_fields(frames, cfg.B, cfg.p)]
     for a, b in zip(got, ref):
         np.testing.assert_array_equal(a, b)
+
+
+def _flat_worker(rank, world, port, frames, B, p, out_q):
+    """Weak-scaling layout of bench.py: every rank searches its own n pairs into one flat
+    buffer and the buffers are all_gathered as they are."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = frames.shape[0] // world
+    nb = (frames.shape[3] // B) * (frames.shape[2] // B)
+    buf = mdist.alloc_flat(n, nb, "cpu")
+    mv, sad, pts, st = mdist.flat_views(buf, n, nb)
+    omv, osad, opts, ost = _oracle_fields(frames[rank * n:(rank + 1) * n], B, p)
+    mv.copy_(omv); sad.copy_(osad); pts.copy_(opts); st.copy_(ost)
+    out = mdist.alloc_flat(n, nb, "cpu", world)
+    mdist.gather_flat(buf, out)
+    if rank == 0:
+        parts = mdist.unpack_gathered(out, n, nb)
+        out_q.put([torch.cat([pr[k] for pr in parts]).numpy() for k in range(4)])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_flat_layout_alignment():
+    for n, nb in [(1, 99), (3, 7), (239, 32640)]:
+        o_mv, o_sad, o_pts, o_st, total = mdist.flat_layout(n, nb)
+        assert o_sad % 4 == 0 and o_pts % 2 == 0 and o_st % 8 == 0 and total >= o_st + 24 * n
+
+
+def test_gloo_flat_gather_matches_single_rank():
+    world, n = 2, 2
+    cfg = synth.CONFIGS["c1"]
+    frames = synth.make_sequence(cfg, pairs=range(1, world * n + 1)).numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_flat_worker, args=(r, world, port, frames, cfg.B, cfg.p, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    ref = [t.numpy() for t in _oracle_fields(frames, cfg.B, cfg.p)]
+    for a, b in zip(got, ref):
+        np.testing.assert_array_equal(a, b)
