@@ -20,10 +20,12 @@ struct FsArgs {
     int W, H, p;
     int tbx, tby, ntx;      // tile of blocks per CTA, tiles per row
     int pitch, rh;          // staged region (TMA box) width / rows
+    int rh_pad;             // rows of each byte-phase copy (>= rh; rows past rh are padding)
     int cstride;            // bytes between byte-phase copies (cstride/4 = 8 mod 32 words)
     int cur_off;            // byte offset of the current tile in shared memory
     int nbx, nb;
     int nch;                // dy chunks of B candidates: ceil((2p+1) / B)
+    int nsplit;             // a (block, dx) item's chunks are split over nsplit thread items
     uint32_t* mv;
     uint32_t* sad;
     uint16_t* pts;
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(256)
     // byte-phase copies 1..3 of the region (copy k word q = region bytes 4q+k .. 4q+k+3)
     {
         const uint32_t* c0 = reinterpret_cast<const uint32_t*>(sref);
-        const int nw = pitch * a.rh / 4;
+        const int nw = pitch * a.rh_pad / 4;
         for (int q = threadIdx.x; q < nw; q += blockDim.x) {
             const uint32_t lo = c0[q], hi = (q + 1 < nw) ? c0[q + 1] : 0u;
 #pragma unroll
@@ -83,16 +85,19 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
 
-    const int nitem = nbt * side * a.nch;
+    // Thread items are (block, dx, split); each loops over its share of the ceil((2p+1)/B)
+    // chunks of B consecutive dy with the current block held in registers.  Staged rows are padded (rh_pad) so the
+    // row loop needs no bounds check: rows past the window only feed candidates dy > p, which
+    // are masked out of the key.
+    const int nsplit = a.nsplit, cps = (a.nch + nsplit - 1) / nsplit;  // chunks per item
+    const int nitem = nbt * side * nsplit;
     const uint32_t* sw = reinterpret_cast<const uint32_t*>(sref);
     const int cwords = a.cstride >> 2, pw = pitch >> 2;
     for (int it = threadIdx.x; it < nitem; it += blockDim.x) {
-        const int per_blk = side * a.nch;
-        const int b = it / per_blk;
-        const int rem = it - b * per_blk;
-        const int c = rem / side;
-        const int dxp = rem - c * side;  // dx + p
-        const int lbx = b % tbx_e, lby = b / tbx_e;
+        const int bs = it / side;
+        const int dxp = it - bs * side;  // dx + p
+        const int b = bs / nsplit, sp = bs - b * nsplit;
+        const int lby = b / tbx_e, lbx = b - lby * tbx_e;
         uint32_t cw[B][W4];
 #pragma unroll
         for (int i = 0; i < B; i++)
@@ -102,39 +107,38 @@ __global__ void __launch_bounds__(256)
         // candidate (dx, dy) block row i sits at region row lby*B + dy + p + i, column
         // (x0 + lbx*B - p - xs) + dx + p
         const int col = (x0 + lbx * B - p - xs) + dxp;
-        const uint32_t* base = sw + (col & 3) * cwords + (col >> 2);
-        const int row0 = lby * B + c * B;  // region row of (dy = c*B - p, i = 0)
-        const int nrow = a.rh;
-        uint32_t acc[B];
+        const uint32_t* base = sw + (col & 3) * cwords + (col >> 2) + (lby * B) * pw;
+        uint32_t key = 0xffffffffu;
+        const int c1 = min(a.nch, (sp + 1) * cps);
+        for (int c = sp * cps; c < c1; c++) {
+            const uint32_t* rb = base + (c * B) * pw;  // region row of (dy = c*B - p, i = 0)
+            uint32_t acc[B];
 #pragma unroll
-        for (int d = 0; d < B; d++) acc[d] = 0;
+            for (int d = 0; d < B; d++) acc[d] = 0;
 #pragma unroll
-        for (int y = 0; y < 2 * B - 1; y++) {
-            const int rr = row0 + y;
-            uint32_t rw[W4];
-            if (rr < nrow) {
+            for (int y = 0; y < 2 * B - 1; y++) {
+                uint32_t rw[W4];
 #pragma unroll
-                for (int w = 0; w < W4; w++) rw[w] = base[rr * pw + w];
-            } else {
+                for (int w = 0; w < W4; w++) rw[w] = rb[y * pw + w];
 #pragma unroll
-                for (int w = 0; w < W4; w++) rw[w] = 0;
-            }
+                for (int d = 0; d < B; d++) {
+                    const int i = y - d;
+                    if (i >= 0 && i < B) {
 #pragma unroll
-            for (int d = 0; d < B; d++) {
-                const int i = y - d;
-                if (i >= 0 && i < B) {
-#pragma unroll
-                    for (int w = 0; w < W4; w++) acc[d] = vsad4(cw[i][w], rw[w], acc[d]);
+                        for (int w = 0; w < W4; w++) acc[d] = vsad4(cw[i][w], rw[w], acc[d]);
+                    }
                 }
             }
-        }
-        uint32_t key = 0xffffffffu;
+            // ranks (reading C13): (0,0) -> 0, else 1 + (dy+p)(2p+1) + (dx+p)
+            const int nd = min(B, side - c * B);
+            const int cd = dxp == p ? p - c * B : -1;  // slot of (0,0) in this chunk, if any
+            const uint32_t r0 = (uint32_t)(1 + c * B * side + dxp);
 #pragma unroll
-        for (int d = 0; d < B; d++) {
-            const int dyp = c * B + d;  // dy + p
-            if (dyp < side) {
-                const uint32_t rank = (dxp == p && dyp == p) ? 0u : (uint32_t)(1 + dyp * side + dxp);
-                key = min(key, (acc[d] << 13) | rank);
+            for (int d = 0; d < B; d++) {
+                if (d < nd) {
+                    const uint32_t rank = d == cd ? 0u : r0 + (uint32_t)(d * side);
+                    key = min(key, (acc[d] << 13) | rank);
+                }
             }
         }
         atomicMin(&s_key[b], key);

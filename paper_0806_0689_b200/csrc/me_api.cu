@@ -278,12 +278,23 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
     const int B = block, nbx = W / B, nby = H / B, side = 2 * p + 1;
     a.W = W; a.H = H; a.p = p;
     a.nch = (side + B - 1) / B;
-    // tile: enough (block, dx, chunk) items for 256 threads, region <= 256 x 256 (TMA box)
-    int tbx = 1, tby = 1;
-    while (tbx * tby * side * a.nch < 1024 && tbx * tby < 64) {
-        if (tbx <= tby && (tbx * 2) * B + 2 * p + 31 <= 240) tbx *= 2;
-        else if ((tby * 2) * B + 2 * p <= 256) tby *= 2;
-        else break;
+    // tile (measured on B200, profiles/r1b/SUMMARY.md): 8x4 blocks for B=8, 4x4 for B=16,
+    // halved while the region exceeds the 256 x 256 TMA box or its 4 byte-phase copies exceed
+    // the shared memory of a CTA
+    int tbx = B == 16 ? 4 : 8, tby = 4;
+    auto fs_smem = [&](int tx, int ty) {
+        const int pt = ((tx * B + 2 * p + 31) + 15) & ~15;
+        const int rp = std::max(ty * B + 2 * p, (ty + a.nch) * B - 1);
+        return 4 * ((pt * rp + 127 + 128 * 4) & ~127) + tx * ty * B * B + 1024;
+    };
+    while ((tbx > 1 || tby > 1) &&
+           (tbx * B + 2 * p + 31 > 256 || tby * B + 2 * p > 256 || fs_smem(tbx, tby) > g_smem_optin - 1024)) {
+        if (tbx >= tby && tbx > 1) tbx /= 2;
+        else tby /= 2;
+    }
+    if (const char* e = getenv("ME_FS_TILE")) {
+        int tx = 0, ty = 0;
+        if (sscanf(e, "%d,%d", &tx, &ty) == 2 && tx > 0 && ty > 0) { tbx = tx; tby = ty; }
     }
     tbx = std::min(tbx, nbx);
     tby = std::min(tby, nby);
@@ -294,7 +305,12 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
     const int TW = tbx * B, TH = tby * B;
     a.pitch = ((TW + 2 * p + 31) + 15) & ~15;
     a.rh = TH + 2 * p;
-    const int rbytes = a.pitch * a.rh;
+    a.rh_pad = std::max(a.rh, (tby + a.nch) * B - 1);  // rows the chunked dy loop touches
+    // measured on B200 (profiles/r1b): 8x8 blocks keep a (block, dx) item whole; 16x16 blocks
+    // (64 cur registers, 16 accumulators per item) split it into one item per dy chunk
+    a.nsplit = B == 16 ? a.nch : 1;
+    if (const char* e = getenv("ME_FS_SPLIT")) a.nsplit = std::max(1, std::min(a.nch, atoi(e)));
+    const int rbytes = a.pitch * a.rh_pad;
     // copy stride: >= region, 128-aligned copy 0, stride/4 = 8 (mod 32) words spreads the copies
     int cs = (rbytes + 127) & ~127;
     while (((cs / 4) & 31) != 8) cs += 16;
