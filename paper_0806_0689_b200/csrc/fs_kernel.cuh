@@ -2,10 +2,11 @@
 //
 // Full search evaluates every candidate of the +-p window (reading C9: all (2p+1)^2 are
 // scorable over the edge-replicated reference; P:355 prints NSP 225 for +-7).  Tie rule
-// (reading C13): (0,0) first, then raster order (dy outer, dx inner), strict minimum -- the
-// argmin of the packed key (SAD << 13) | rank with rank(0,0) = 0 and
-// rank(dx,dy) = 1 + (dy+p)(2p+1) + (dx+p) otherwise (SAD <= 65280 and rank <= 4225 keep it in
-// 32 bits for B <= 16, p <= 32).
+// (reading C13): (0,0) first, then raster order (dy outer, dx inner), strict minimum.  The
+// kernel takes the argmin of the packed key (SAD << 13) + rank, rank(dx,dy) = 1 + (dy+p)(2p+1)
+// + (dx+p) for every candidate (SAD <= 65280 and rank <= 4225 keep it in 32 bits for B <= 16,
+// p <= 32) -- the raster-first minimum -- and then applies centre-first once per block: (0,0)
+// is the MV iff its SAD is <= that minimum's.
 //
 // One CTA per tile of blocks: the tile's edge-replicated reference region is staged by TMA
 // (as for DCDS) and expanded into four byte-phase copies; see fs_kernel below.
@@ -129,16 +130,17 @@ __global__ void __launch_bounds__(256)
                     }
                 }
             }
-            // ranks (reading C13): (0,0) -> 0, else 1 + (dy+p)(2p+1) + (dx+p)
-            const int nd = min(B, side - c * B);
-            const int cd = dxp == p ? p - c * B : -1;  // slot of (0,0) in this chunk, if any
+            // raster ranks 1 + (dy+p)(2p+1) + (dx+p) for every candidate, (0,0) included; the
+            // centre-first rule (reading C13) is applied once per block in the output phase
             const uint32_t r0 = (uint32_t)(1 + c * B * side + dxp);
+            if ((c + 1) * B <= side) {
 #pragma unroll
-            for (int d = 0; d < B; d++) {
-                if (d < nd) {
-                    const uint32_t rank = d == cd ? 0u : r0 + (uint32_t)(d * side);
-                    key = min(key, (acc[d] << 13) | rank);
-                }
+                for (int d = 0; d < B; d++) key = min(key, (acc[d] << 13) + (r0 + (uint32_t)(d * side)));
+            } else {  // the last chunk: rows past dy = p are padding
+                const int nd = side - c * B;
+#pragma unroll
+                for (int d = 0; d < B; d++)
+                    if (d < nd) key = min(key, (acc[d] << 13) + (r0 + (uint32_t)(d * side)));
             }
         }
         atomicMin(&s_key[b], key);
@@ -147,11 +149,23 @@ __global__ void __launch_bounds__(256)
     // outputs + SSE at the FS MV (per-pair statistics), one warp per block
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int b = warp; b < nbt; b += nw) {
-        const uint32_t k2 = s_key[b];
+        const int lbx = b % tbx_e, lby = b / tbx_e;
+        // centre first (reading C13): (0,0) is the MV unless another candidate is strictly
+        // cheaper; the raster-first minimum of the others is the key's candidate
+        const int col0 = x0 + lbx * B - xs;
+        const uint32_t* base0 = sw + (col0 & 3) * cwords + (col0 >> 2);
+        uint32_t s0 = 0;
+        for (int e = lane; e < B * W4; e += 32) {
+            const int i = e / W4, w = e - i * W4;
+            const uint32_t cv = reinterpret_cast<const uint32_t*>(scur + (lby * B + i) * TW + lbx * B)[w];
+            s0 = vsad4(cv, base0[(lby * B + p + i) * pw + w], s0);
+        }
+        s0 = __reduce_add_sync(FULL, s0);
+        uint32_t k2 = s_key[b];
+        if ((k2 >> 13) >= s0) k2 = s0 << 13;  // rank 0 = the centre
         const uint32_t rank = k2 & 0x1fffu;
         const int cidx = rank == 0 ? p * side + p : (int)rank - 1;
         const int mdy = cidx / side - p, mdx = cidx % side - p;
-        const int lbx = b % tbx_e, lby = b / tbx_e;
         uint32_t sse = 0;
         const int col = (x0 + lbx * B - p - xs) + mdx + p;
         const uint32_t* base = sw + (col & 3) * cwords + (col >> 2);
