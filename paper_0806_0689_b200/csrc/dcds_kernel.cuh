@@ -370,9 +370,7 @@ __global__ void __launch_bounds__(NWARP * 32)
     dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
                 const SearchArgs a) {
     static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "lane-group size");
-    constexpr int R = B / G;      // rows per lane (lane j of a group: rows j, j+G, ...)
-    constexpr int W4 = B / 4;     // 32-bit words per block row
-    constexpr int NG = 32 / G;    // groups per warp
+    constexpr int NG = 32 / G;    // groups per warp (rows per lane and words per row: GroupState)
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ int4 s_poff[8];
     __shared__ uint32_t s_pcode[8];

@@ -40,8 +40,6 @@ struct HostStage {
 };
 HostStage g_stage[2];
 
-constexpr int kNWarp = 4;
-
 int set_cuda_err(cudaError_t e, const char* where) {
     snprintf(g_err, sizeof g_err, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
     return ME_ECUDA;
