@@ -144,6 +144,38 @@ __device__ __forceinline__ void ref_rows(const uint32_t* s, int o, int rstride,
     }
 }
 
+// W4+2 words around an ALIGNED row start a (a multiple of 4*W4 bytes: one vector load of
+// the row): w[0] = the word before, w[1..W4] = the row, w[W4+1] = the word after.
+template <int W4>
+__device__ __forceinline__ void aligned_row(const uint32_t* s, int a, uint32_t (&w)[W4 + 2]) {
+    const uint32_t* b = s + (a >> 2);
+    w[0] = b[-1];
+    if (W4 == 2) {
+        const uint2 v = *reinterpret_cast<const uint2*>(b);
+        w[1] = v.x; w[2] = v.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < W4; q += 4) {
+            const uint4 v = *reinterpret_cast<const uint4*>(b + q);
+            w[1 + q] = v.x; w[2 + q] = v.y; w[3 + q] = v.z; w[4 + q] = v.w;
+        }
+    }
+    w[W4 + 1] = b[W4];
+}
+// SAD of one row against the reference shifted by t bytes (t in [-3, 3]) from an aligned_row.
+template <int W4>
+__device__ __forceinline__ uint32_t sad_shift(const uint32_t (&c)[W4], const uint32_t (&w)[W4 + 2],
+                                              int t, uint32_t acc) {
+#pragma unroll
+    for (int i = 0; i < W4; i++) {
+        const uint32_t r = t == 0 ? w[i + 1]
+                          : t > 0 ? __funnelshift_r(w[i + 1], w[i + 2], 8 * t)
+                                  : __funnelshift_r(w[i], w[i + 1], 8 * (4 + t));
+        acc = vsad4(c[i], r, acc);
+    }
+    return acc;
+}
+
 // Offsets of the DDSP points in the fixed order (reading C7), candidate k = 0..3.
 //   HDSP: (-2,0) (2,0) (0,-1) (0,1)      VDSP: (-1,0) (1,0) (0,-2) (0,2)
 __device__ __forceinline__ int ddsp_dx(int kind, int k) {
@@ -275,19 +307,51 @@ struct GroupState {
 
         // ---- SADs of the 4 slots over this lane's rows, packed and reduced over the group
         const int ok[4] = {po.x, po.y, po.z, po.w};
-        uint32_t sadk[4];
+        uint32_t sadk[4] = {0u, 0u, 0u, 0u};
+        // 16x16 blocks: Step 1 runs at the window origin, whose staged address is aligned (x0 - xs
+        // and the block column are multiples of 16), so its points come from aligned row loads
+        // with static shifts (measured on B200: -10 % at c4; for 8x8 blocks the extra path costs
+        // more than it saves, profiles/r1b/SUMMARY.md).  Infeasible slots are masked out by m4.
+        constexpr bool kS1Aligned = (B == 16);
+        const bool quiet = (st >= ST_IDLE || st == ST_DONE);
+        if (kS1Aligned && __all_sync(FULL, quiet || st == ST_S1A)) {
+            // (0,0) (-1,0) (1,0) (-2,0): one aligned row load per row
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            uint32_t acc = 0;
-            if ((m4 >> k) & 1) {  // slots not scored this pass issue no shared-memory loads
-                uint32_t rw[R][W4];
-                ref_rows<R, W4>(s, cpos + ok[k] + jrow, rstride, rw);
-#pragma unroll
-                for (int r = 0; r < R; r++)
-#pragma unroll
-                    for (int w = 0; w < W4; w++) acc = vsad4(cw[r][w], rw[r][w], acc);
+            for (int r = 0; r < R && !quiet; r++) {
+                uint32_t w[W4 + 2];
+                aligned_row<W4>(s, bofs + jrow + r * rstride, w);
+                sadk[0] = sad_shift<W4>(cw[r], w, 0, sadk[0]);
+                sadk[1] = sad_shift<W4>(cw[r], w, -1, sadk[1]);
+                sadk[2] = sad_shift<W4>(cw[r], w, 1, sadk[2]);
+                sadk[3] = sad_shift<W4>(cw[r], w, -2, sadk[3]);
             }
-            sadk[k] = acc;
+        } else if (kS1Aligned && __all_sync(FULL, quiet || st == ST_S1B)) {
+            // (2,0) (0,-1) (0,1): aligned rows
+#pragma unroll
+            for (int r = 0; r < R && !quiet; r++) {
+                const int a = bofs + jrow + r * rstride;
+                uint32_t w[W4 + 2], u[W4 + 2], d[W4 + 2];
+                aligned_row<W4>(s, a, w);
+                aligned_row<W4>(s, a - pitch, u);
+                aligned_row<W4>(s, a + pitch, d);
+                sadk[0] = sad_shift<W4>(cw[r], w, 2, sadk[0]);
+                sadk[1] = sad_shift<W4>(cw[r], u, 0, sadk[1]);
+                sadk[2] = sad_shift<W4>(cw[r], d, 0, sadk[2]);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                uint32_t acc = 0;
+                if ((m4 >> k) & 1) {  // slots not scored this pass issue no shared-memory loads
+                    uint32_t rw[R][W4];
+                    ref_rows<R, W4>(s, cpos + ok[k] + jrow, rstride, rw);
+#pragma unroll
+                    for (int r = 0; r < R; r++)
+#pragma unroll
+                        for (int w = 0; w < W4; w++) acc = vsad4(cw[r][w], rw[r][w], acc);
+                }
+                sadk[k] = acc;
+            }
         }
         uint32_t v01 = sadk[0] | (sadk[1] << 16), v23 = sadk[2] | (sadk[3] << 16);
 #pragma unroll

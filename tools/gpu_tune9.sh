@@ -1,0 +1,7 @@
+# usage: bash tools/gpu_tune9.sh "<cfg> <G> <tile> <NW> <OPT>" ...   (DCDS engine knobs)
+for spec in "$@"; do
+  set -- $spec
+  out=gpurun_out/tune_$1_$2_$3_$4_o$5.json
+  ME_G=$2 ME_TILE=$3 ME_NW=$4 ME_OPT=$5 timeout 300 python bench.py --config $1 --steps 20 --warmup 3 --no-fs --no-e2e --no-cpu --no-cmp > $out 2>&1
+  echo "$spec $(python -c "import json;d=json.load(open('$out'));print(round(d['ms_per_step'],3), '%.3e'%d['value'], round(d['roofline']['frac'],4))" 2>&1 | tail -1)"
+done
