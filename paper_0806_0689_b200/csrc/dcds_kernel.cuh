@@ -262,6 +262,70 @@ struct GroupState {
         key1 = 0xffffffffu;
     }
 
+    // Step 1 of a block that starts it now (st == ST_S1A), in one straight-line
+    // pass: the HCSP points (0,0) (-1,0) (1,0) (-2,0) (2,0) (0,-1) (0,1) (reading C7 order)
+    // come from aligned vector row loads with static shifts -- the pattern centre is the
+    // window origin, whose staged address is a multiple of 4*W4 bytes for every block.  Ends
+    // in Step 3 (switching strategy one) or, on the halfway stop, in a Step-4
+    // state with no slots, which the next pass finishes.  All lanes of the warp call it (and
+    // __syncwarp after it).
+    __device__ __forceinline__ void step1(const uint32_t* s, uint32_t* bm, int j, int p, int pitch,
+                                          int rstride, int jrow) {
+        const bool live = (st == ST_S1A);
+        uint32_t sk[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        if (live) {
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const int a = bofs + jrow + r * rstride;
+                uint32_t w[W4 + 2], u[W4 + 2], d[W4 + 2];
+                aligned_row<W4>(s, a, w);
+                aligned_row<W4>(s, a - pitch, u);
+                aligned_row<W4>(s, a + pitch, d);
+                sk[0] = sad_shift<W4>(cw[r], w, 0, sk[0]);
+                sk[1] = sad_shift<W4>(cw[r], w, -1, sk[1]);
+                sk[2] = sad_shift<W4>(cw[r], w, 1, sk[2]);
+                sk[3] = sad_shift<W4>(cw[r], w, -2, sk[3]);
+                sk[4] = sad_shift<W4>(cw[r], w, 2, sk[4]);
+                sk[5] = sad_shift<W4>(cw[r], u, 0, sk[5]);
+                sk[6] = sad_shift<W4>(cw[r], d, 0, sk[6]);
+            }
+        }
+        uint32_t v[4] = {sk[0] | (sk[1] << 16), sk[2] | (sk[3] << 16), sk[4] | (sk[5] << 16), sk[6]};
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1)
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] += __shfl_xor_sync(FULL, v[q], o);
+        if (!live) return;
+        // feasibility (reading C8): only (+-2,0) can leave the window (p = 1)
+        const unsigned feas = p >= 2 ? 0x7fu : 0x67u;
+        uint32_t key = 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < 7; k++) {
+            const uint32_t sad = (v[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+            if ((feas >> k) & 1) key = min(key, (sad << 3) | k);
+        }
+        // visited set (reading C5): the group's first lane marks the scored points
+        if (j == 0) {
+            const int side = 2 * p + 1, c = p * side + p;
+            const int idx[7] = {c, c - 1, c + 1, c - 2, c + 2, c - side, c + side};
+#pragma unroll
+            for (int k = 0; k < 7; k++)
+                if ((feas >> k) & 1) bm[idx[k] >> 5] |= 1u << (idx[k] & 31);
+        }
+        pts = __popc(feas);
+        best = key >> 3;
+        const int kb = key & 7;
+        if (kb == 0) {  // halfway stop: finish with no further slots
+            st = ST_S4; pid = 4; want = 0;
+        } else {
+            cx = hcsp_dx(kb);
+            cy = hcsp_dy(kb);
+            cpos = bofs + cy * pitch + cx;
+            kind = (cy == 0) ? 0 : 1;  // switching strategy one
+            st = ST_S3; pid = 2 + kind;
+        }
+    }
+
     // SSE (P:342 aspect 4) of this lane's rows at the current centre.
     __device__ __forceinline__ uint32_t sse_rows(const uint32_t* s, int jrow, int rstride) const {
         uint32_t rw[R][W4];
@@ -307,51 +371,19 @@ struct GroupState {
 
         // ---- SADs of the 4 slots over this lane's rows, packed and reduced over the group
         const int ok[4] = {po.x, po.y, po.z, po.w};
-        uint32_t sadk[4] = {0u, 0u, 0u, 0u};
-        // 16x16 blocks: Step 1 runs at the window origin, whose staged address is aligned (x0 - xs
-        // and the block column are multiples of 16), so its points come from aligned row loads
-        // with static shifts (measured on B200: -10 % at c4; for 8x8 blocks the extra path costs
-        // more than it saves, profiles/r1b/SUMMARY.md).  Infeasible slots are masked out by m4.
-        constexpr bool kS1Aligned = (B == 16);
-        const bool quiet = (st >= ST_IDLE || st == ST_DONE);
-        if (kS1Aligned && __all_sync(FULL, quiet || st == ST_S1A)) {
-            // (0,0) (-1,0) (1,0) (-2,0): one aligned row load per row
+        uint32_t sadk[4];
 #pragma unroll
-            for (int r = 0; r < R && !quiet; r++) {
-                uint32_t w[W4 + 2];
-                aligned_row<W4>(s, bofs + jrow + r * rstride, w);
-                sadk[0] = sad_shift<W4>(cw[r], w, 0, sadk[0]);
-                sadk[1] = sad_shift<W4>(cw[r], w, -1, sadk[1]);
-                sadk[2] = sad_shift<W4>(cw[r], w, 1, sadk[2]);
-                sadk[3] = sad_shift<W4>(cw[r], w, -2, sadk[3]);
+        for (int k = 0; k < 4; k++) {
+            uint32_t acc = 0;
+            if ((m4 >> k) & 1) {  // slots not scored this pass issue no shared-memory loads
+                uint32_t rw[R][W4];
+                ref_rows<R, W4>(s, cpos + ok[k] + jrow, rstride, rw);
+#pragma unroll
+                for (int r = 0; r < R; r++)
+#pragma unroll
+                    for (int w = 0; w < W4; w++) acc = vsad4(cw[r][w], rw[r][w], acc);
             }
-        } else if (kS1Aligned && __all_sync(FULL, quiet || st == ST_S1B)) {
-            // (2,0) (0,-1) (0,1): aligned rows
-#pragma unroll
-            for (int r = 0; r < R && !quiet; r++) {
-                const int a = bofs + jrow + r * rstride;
-                uint32_t w[W4 + 2], u[W4 + 2], d[W4 + 2];
-                aligned_row<W4>(s, a, w);
-                aligned_row<W4>(s, a - pitch, u);
-                aligned_row<W4>(s, a + pitch, d);
-                sadk[0] = sad_shift<W4>(cw[r], w, 2, sadk[0]);
-                sadk[1] = sad_shift<W4>(cw[r], u, 0, sadk[1]);
-                sadk[2] = sad_shift<W4>(cw[r], d, 0, sadk[2]);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                uint32_t acc = 0;
-                if ((m4 >> k) & 1) {  // slots not scored this pass issue no shared-memory loads
-                    uint32_t rw[R][W4];
-                    ref_rows<R, W4>(s, cpos + ok[k] + jrow, rstride, rw);
-#pragma unroll
-                    for (int r = 0; r < R; r++)
-#pragma unroll
-                        for (int w = 0; w < W4; w++) acc = vsad4(cw[r][w], rw[r][w], acc);
-                }
-                sadk[k] = acc;
-            }
+            sadk[k] = acc;
         }
         uint32_t v01 = sadk[0] | (sadk[1] << 16), v23 = sadk[2] | (sadk[3] << 16);
 #pragma unroll
@@ -490,6 +522,27 @@ __global__ void __launch_bounds__(NWARP * 32)
     GroupState<B, G> gs;  // group state (every lane of a group holds the same values)
     long long gblk = 0;
     unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
+
+    // ---- every group's first block of the tile runs Step 1 straight away (aligned loads)
+    {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(ctr, NG);
+        base = __shfl_sync(FULL, base, 0);
+        const int idx = base + g;
+        if (idx < nbt) {
+            const int lby = (int)(((float)idx + 0.5f) * inv_tbx);
+            const int lbx = idx - lby * tbx_e;
+            const int bxg = x0 + lbx * B, byg = y0 + lby * B;
+            gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
+            gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW,
+                     j, bm, a.bm_words);
+        } else {
+            gs.st = ST_IDLE;
+        }
+        __syncwarp();
+        gs.step1(s, bm, j, p, pitch, rstride, jrow);
+        __syncwarp();  // the visited bits are set before any pass tests them
+    }
 
     for (;;) {
         // ---- groups that are done take the next block of the tile
