@@ -240,7 +240,7 @@ struct GroupState {
     static constexpr int W4 = B / 4;  // 32-bit words per block row
     int st = ST_DONE, pid = 0, kind = 0, cx = 0, cy = 0, pts = 0, want = 3;
     int bofs = 0, cpos = 0;
-    uint32_t best = 0, s0 = 0, key1 = 0xffffffffu;
+    uint32_t best = 0;
     uint32_t cw[R][W4];
 
     // Start the search of the block whose (0,0) candidate is at byte `origin` of the staged
@@ -259,7 +259,6 @@ struct GroupState {
         for (int w = j * 4; w < bm_words; w += 4 * G)
             *reinterpret_cast<uint4*>(bm + w) = make_uint4(0, 0, 0, 0);
         st = ST_S1A; pid = 0; kind = 0; cx = 0; cy = 0; pts = 0; want = 3;
-        key1 = 0xffffffffu;
     }
 
     // Step 1 of a block that starts it now (st == ST_S1A), in one straight-line
@@ -406,31 +405,7 @@ struct GroupState {
         // ---- advance the state machine (group-uniform)
         bool fin = false;
         if (st != ST_S4PRE) pts += __popc(m4);
-        if (st == ST_S1A) {
-            // Step 1, first half: the centre (slot 0) is the incumbent
-            s0 = sadk[0];
-            uint32_t kk = 0xffffffffu;
-#pragma unroll
-            for (int k = 1; k < 4; k++)
-                if ((m4 >> k) & 1) kk = min(kk, (sadk[k] << 3) | k);
-            key1 = kk;
-            st = ST_S1B; pid = 1;
-        } else if (st == ST_S1B) {
-            uint32_t kk = key1;
-            if (key != 0xffffffffu) kk = min(kk, ((key >> 2) << 3) | (4 + kb));
-            if ((kk >> 3) < s0) {
-                best = kk >> 3;
-                const int h = kk & 7;
-                cx = hcsp_dx(h);
-                cy = hcsp_dy(h);
-                cpos = bofs + cy * pitch + cx;
-                kind = (cy == 0) ? 0 : 1;  // switching strategy one
-                st = ST_S3; pid = 2 + kind;
-            } else {  // halfway stop
-                best = s0;
-                fin = true;
-            }
-        } else if (st == ST_S3) {
+        if (st == ST_S3) {
             // Step 2 / Step 3
             if ((key >> 2) < best) {
                 best = key >> 2;
@@ -523,27 +498,6 @@ __global__ void __launch_bounds__(NWARP * 32)
     long long gblk = 0;
     unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
 
-    // ---- every group's first block of the tile runs Step 1 straight away (aligned loads)
-    {
-        int base = 0;
-        if (lane == 0) base = atomicAdd(ctr, NG);
-        base = __shfl_sync(FULL, base, 0);
-        const int idx = base + g;
-        if (idx < nbt) {
-            const int lby = (int)(((float)idx + 0.5f) * inv_tbx);
-            const int lbx = idx - lby * tbx_e;
-            const int bxg = x0 + lbx * B, byg = y0 + lby * B;
-            gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
-            gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW,
-                     j, bm, a.bm_words);
-        } else {
-            gs.st = ST_IDLE;
-        }
-        __syncwarp();
-        gs.step1(s, bm, j, p, pitch, rstride, jrow);
-        __syncwarp();  // the visited bits are set before any pass tests them
-    }
-
     for (;;) {
         // ---- groups that are done take the next block of the tile
         const bool need = (gs.st == ST_DONE);
@@ -570,6 +524,11 @@ __global__ void __launch_bounds__(NWARP * 32)
             __syncwarp();
         }
         if (__all_sync(FULL, gs.st == ST_IDLE)) break;
+        // ---- groups that just took a block run Step 1 in one straight-line step
+        if (__any_sync(FULL, gs.st == ST_S1A)) {
+            gs.step1(s, bm, j, p, pitch, rstride, jrow);
+            __syncwarp();  // the visited bits are set before the pass tests them
+        }
 
         const bool fin = gs.template pass<VARIANT>(s, bm, s_pcode, s_poff, j, leader, p, pitch, rstride, jrow);
 
