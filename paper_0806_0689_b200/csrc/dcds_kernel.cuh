@@ -104,15 +104,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 // copies the nearest in-frame row into out-of-frame rows.  Border tiles only.
 __device__ __forceinline__ void fixup_edges(uint8_t* sref, int pitch, int rh, int xs, int ys,
                                             int W, int H) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int i0 = max(0, -ys), i1 = min(rh, H - ys);      // in-frame rows [i0, i1)
     const int cl = max(0, -xs), cr = min(pitch, W - xs);    // in-frame cols [cl, cr)
     if (cl > 0 || cr < pitch) {
-        for (int i = i0 + warp; i < i1; i += nw) {
+        // xs, W and pitch are multiples of 16: the out-of-frame column spans are whole uint4s
+        const int nl = cl >> 4, nr = (pitch - cr) >> 4;
+        for (int e = threadIdx.x; e < (i1 - i0) * (nl + nr); e += blockDim.x) {
+            const int i = i0 + e / (nl + nr), q = e % (nl + nr);
             uint8_t* row = sref + i * pitch;
-            const uint8_t vl = row[cl], vr = row[cr - 1];
-            for (int c = lane; c < cl; c += 32) row[c] = vl;
-            for (int c = cr + lane; c < pitch; c += 32) row[c] = vr;
+            const uint32_t v = (q < nl ? row[cl] : row[cr - 1]) * 0x01010101u;
+            reinterpret_cast<uint4*>(row)[q < nl ? q : (cr >> 4) + (q - nl)] = make_uint4(v, v, v, v);
         }
     }
     __syncthreads();
@@ -354,7 +355,8 @@ struct GroupState {
             bool nw = false;
             if (k < 4 && ((used >> k) & 1)) {
                 const int qx = cx + code_dx(pw, k), qy = cy + code_dy(pw, k);
-                if (qx >= -p && qx <= p && qy >= -p && qy <= p) {  // window only (reading C8)
+                if ((unsigned)(qx + p) <= (unsigned)(2 * p) &&
+                    (unsigned)(qy + p) <= (unsigned)(2 * p)) {  // window only (reading C8)
                     if (st == ST_S4PRE) {
                         nw = true;  // DCDS^S look-up of the distant points: not scored again
                     } else {
@@ -400,7 +402,7 @@ struct GroupState {
             if ((m4 >> k) & 1) key = min(key, (sadk[k] << 2) | k);
         const int kb = key & 3;
         const int mdx = code_dx(pw, kb), mdy = code_dy(pw, kb);
-        const int mo = kb == 0 ? po.x : kb == 1 ? po.y : kb == 2 ? po.z : po.w;
+        const int mo = mdy * pitch + mdx;
 
         // ---- advance the state machine (group-uniform)
         bool fin = false;
@@ -492,7 +494,6 @@ __global__ void __launch_bounds__(NWARP * 32)
     const int nby = a.nb / a.nbx;
     const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, nby - ty * a.tby);
     const int nbt = tbx_e * tby_e;
-    const float inv_tbx = 1.0f / (float)tbx_e;
 
     GroupState<B, G> gs;  // group state (every lane of a group holds the same values)
     long long gblk = 0;
@@ -510,8 +511,7 @@ __global__ void __launch_bounds__(NWARP * 32)
             idx = __shfl_sync(FULL, idx, leader);
             if (need) {
                 if (idx < nbt) {
-                    // idx / tbx_e in float is exact here: idx < 2^16, tbx_e <= 2^8
-                    const int lby = (int)(((float)idx + 0.5f) * inv_tbx);
+                    const int lby = idx / tbx_e;
                     const int lbx = idx - lby * tbx_e;
                     const int bxg = x0 + lbx * B, byg = y0 + lby * B;
                     gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
