@@ -239,7 +239,8 @@ template <int B, int G>
 struct GroupState {
     static constexpr int R = B / G;   // rows per lane (lane j of a group: rows j, j+G, ...)
     static constexpr int W4 = B / 4;  // 32-bit words per block row
-    int st = ST_DONE, pid = 0, kind = 0, cx = 0, cy = 0, pts = 0, want = 3;
+    int st = ST_DONE, pid = 0, kind = 0, cx = 0, cy = 0, pts = 0;
+    int want = 0;  // slot mask of the next pass (0 when done / idle)
     int bofs = 0, cpos = 0;
     uint32_t best = 0;
     uint32_t cw[R][W4];
@@ -257,9 +258,10 @@ struct GroupState {
 #pragma unroll
             for (int w = 0; w < W4; w++) cw[r][w] = crow[w];
         }
+#pragma unroll 4
         for (int w = j * 4; w < bm_words; w += 4 * G)
             *reinterpret_cast<uint4*>(bm + w) = make_uint4(0, 0, 0, 0);
-        st = ST_S1A; pid = 0; kind = 0; cx = 0; cy = 0; pts = 0; want = 3;
+        st = ST_S1A; pid = 0; kind = 0; cx = 0; cy = 0; pts = 0; want = 0xf;
     }
 
     // Step 1 of a block that starts it now (st == ST_S1A), in one straight-line
@@ -322,7 +324,7 @@ struct GroupState {
             cy = hcsp_dy(kb);
             cpos = bofs + cy * pitch + cx;
             kind = (cy == 0) ? 0 : 1;  // switching strategy one
-            st = ST_S3; pid = 2 + kind;
+            st = ST_S3; pid = 2 + kind; want = 0xf;
         }
     }
 
@@ -345,7 +347,7 @@ struct GroupState {
                                          int rstride, int jrow) {
         const uint32_t pw = s_pcode[pid];
         const int4 po = s_poff[pid];
-        const uint32_t used = (st >= ST_IDLE || st == ST_DONE) ? 0u : ((pw >> 24) & (st == ST_S4 ? (uint32_t)want : 0xfu));
+        const uint32_t used = (pw >> 24) & (uint32_t)want;
 
         // ---- visited-set test-and-set (reading C5): lane j of a group owns slots j, j+G, ...
         unsigned m4 = 0;
@@ -518,7 +520,7 @@ __global__ void __launch_bounds__(NWARP * 32)
                     gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW,
                              j, bm, a.bm_words);
                 } else {
-                    gs.st = ST_IDLE;
+                    gs.st = ST_IDLE; gs.want = 0;
                 }
             }
             __syncwarp();
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(NWARP * 32)
                     acc_sad += gs.best;
                     acc_sse += ss;
                 }
-                gs.st = ST_DONE;
+                gs.st = ST_DONE; gs.want = 0;
             }
         }
     }
