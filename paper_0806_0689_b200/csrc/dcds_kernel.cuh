@@ -496,6 +496,7 @@ __global__ void __launch_bounds__(NWARP * 32)
     const int nby = a.nb / a.nbx;
     const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, nby - ty * a.tby);
     const int nbt = tbx_e * tby_e;
+    const float inv_tbx = __frcp_rn((float)tbx_e);
 
     GroupState<B, G> gs;  // group state (every lane of a group holds the same values)
     long long gblk = 0;
@@ -506,21 +507,28 @@ __global__ void __launch_bounds__(NWARP * 32)
         const bool need = (gs.st == ST_DONE);
         const unsigned ball = __ballot_sync(FULL, need && j == 0);
         if (ball) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(ctr, __popc(ball));
-            base = __shfl_sync(FULL, base, 0);
-            int idx = base + __popc(ball & ((1u << lane) - 1u));
-            idx = __shfl_sync(FULL, idx, leader);
-            if (need) {
-                if (idx < nbt) {
-                    const int lby = idx / tbx_e;
-                    const int lbx = idx - lby * tbx_e;
-                    const int bxg = x0 + lbx * B, byg = y0 + lby * B;
-                    gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
-                    gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW,
-                             j, bm, a.bm_words);
-                } else {
-                    gs.st = ST_IDLE; gs.want = 0;
+            if (*reinterpret_cast<volatile int*>(ctr) >= nbt) {
+                // the tile's blocks are all taken (one shared load, warp-uniform)
+                if (need) { gs.st = ST_IDLE; gs.want = 0; }
+            } else {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(ctr, __popc(ball));
+                base = __shfl_sync(FULL, base, 0);
+                int idx = base + __popc(ball & ((1u << lane) - 1u));
+                idx = __shfl_sync(FULL, idx, leader);
+                if (need) {
+                    if (idx < nbt) {
+                        // idx / tbx_e by the correctly rounded reciprocal: exact for idx < 2^16,
+                        // tbx_e <= 2^8 (the +0.5 keeps the product 0.5/tbx_e from an integer)
+                        const int lby = (int)(((float)idx + 0.5f) * inv_tbx);
+                        const int lbx = idx - lby * tbx_e;
+                        const int bxg = x0 + lbx * B, byg = y0 + lby * B;
+                        gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
+                        gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW,
+                                 j, bm, a.bm_words);
+                    } else {
+                        gs.st = ST_IDLE; gs.want = 0;
+                    }
                 }
             }
             __syncwarp();
