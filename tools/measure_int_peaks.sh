@@ -1,3 +1,4 @@
+# usage: bash tools/measure_int_peaks.sh  -- VABSDIFF4 / IDP.4A / SHF issue rates (profiles/int_peaks.json)
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 120 ./tools/int_peaks > gpurun_out/int_peaks.json; echo "int_peaks rc=$?"
