@@ -94,11 +94,16 @@ __global__ void __launch_bounds__(256)
     const int nitem = nbt * side * nsplit;
     const uint32_t* sw = reinterpret_cast<const uint32_t*>(sref);
     const int cwords = a.cstride >> 2, pw = pitch >> 2;
+    // x / d as floor((x + 1/2) * rcp(d)): exact here (x < 2^14, d <= 65: the product stays
+    // >= 0.5/d from an integer, far above the float rounding error)
+    const float r_side = __frcp_rn((float)side), r_split = __frcp_rn((float)nsplit),
+                r_tbx = __frcp_rn((float)tbx_e);
+    auto fdiv = [](int x, float r) { return (int)(((float)x + 0.5f) * r); };
     for (int it = threadIdx.x; it < nitem; it += blockDim.x) {
-        const int bs = it / side;
+        const int bs = fdiv(it, r_side);
         const int dxp = it - bs * side;  // dx + p
-        const int b = bs / nsplit, sp = bs - b * nsplit;
-        const int lby = b / tbx_e, lbx = b - lby * tbx_e;
+        const int b = fdiv(bs, r_split), sp = bs - b * nsplit;
+        const int lby = fdiv(b, r_tbx), lbx = b - lby * tbx_e;
         uint32_t cw[B][W4];
 #pragma unroll
         for (int i = 0; i < B; i++)
@@ -149,7 +154,7 @@ __global__ void __launch_bounds__(256)
     // outputs + SSE at the FS MV (per-pair statistics), one warp per block
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int b = warp; b < nbt; b += nw) {
-        const int lbx = b % tbx_e, lby = b / tbx_e;
+        const int lby = fdiv(b, r_tbx), lbx = b - lby * tbx_e;
         // centre first (reading C13): (0,0) is the MV unless another candidate is strictly
         // cheaper; the raster-first minimum of the others is the key's candidate
         const int col0 = x0 + lbx * B - xs;
@@ -165,7 +170,8 @@ __global__ void __launch_bounds__(256)
         if ((k2 >> 13) >= s0) k2 = s0 << 13;  // rank 0 = the centre
         const uint32_t rank = k2 & 0x1fffu;
         const int cidx = rank == 0 ? p * side + p : (int)rank - 1;
-        const int mdy = cidx / side - p, mdx = cidx % side - p;
+        const int cq = fdiv(cidx, r_side);
+        const int mdy = cq - p, mdx = cidx - cq * side - p;
         uint32_t sse = 0;
         const int col = (x0 + lbx * B - p - xs) + mdx + p;
         const uint32_t* base = sw + (col & 3) * cwords + (col >> 2);
