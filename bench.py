@@ -232,8 +232,14 @@ def main():
         return run_reference(args)
     ws, rank, local = dist_env()
     if ws > 1:
+        import datetime
+
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # a hung or failed peer aborts the run instead of stalling it (pairs are stateless:
+        # a failed run is simply re-run)
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(minutes=5))
     else:
         dist = None
     torch.cuda.set_device(local)
