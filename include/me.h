@@ -95,6 +95,27 @@ int me_dcds_s_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_strid
                     int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
                     uint16_t* points_out, uint64_t* stats_out);
 
+/* Diagnostic trace of DCDS (variant 0) / DCDS^S (variant 1): the same search as
+ * me_dcds_batch / me_dcds_s_batch (same outputs, bit for bit) from a separately compiled
+ * kernel that also records every scoring pass of every block ("trace"), to diff a
+ * search against the oracle's point-by-point trace when parity fails.  Default lane-group
+ * geometry only (ME_EINVAL when ME_G / ME_NW override it).
+ * trace_out (device) [npairs][nb][trace_cap] uint64, one record per pass in search order:
+ *   bits 0-7   pass number (0 = Step 1, 1..n = Steps 2-3, n+1 = Step 4)
+ *   bits 8-11  pattern: 15 = HCSP (Step 1), 2 = HDSP, 3 = VDSP, 4 / 5 = horizontal / vertical
+ *              middle points (Step 4); the DCDS^S distant-point look-up is not a pass
+ *   bits 12-19 slots newly scored (bit k = slot k of the pattern in the order of reading C7:
+ *              HCSP (0,0) (-1,0) (1,0) (-2,0) (2,0) (0,-1) (0,1); HDSP (-2,0) (2,0) (0,-1)
+ *              (0,1); VDSP (-1,0) (1,0) (0,-2) (0,2); middle points (-1,0) (1,0) / (0,-1) (0,1))
+ *   bits 20-27 / 28-35  pattern centre dx / dy (int8 two's complement)
+ *   bits 36-51 incumbent SAD after the pass
+ * trace_len_out (device) [npairs][nb] uint16: passes of each block (records beyond
+ * trace_cap are counted but not written).  1 <= trace_cap <= 255; trace_out 8-byte aligned. */
+int me_dcds_trace_batch(int variant, const uint8_t* cur0, const uint8_t* ref0,
+                        int64_t pair_stride, int npairs, int W, int H, int block, int p,
+                        int16_t* mv_out, uint32_t* sad_out, uint16_t* points_out,
+                        uint64_t* trace_out, int trace_cap, uint16_t* trace_len_out);
+
 /* Block-matching algorithm ids of me_bma_batch.  DCDS / DCDS^S are the paper's method; the
  * others are the comparison BMAs the paper measures DCDS against (Table VII
  * P:307-324), with the readings of DESIGN.md C23-C26:

@@ -47,6 +47,9 @@ struct SearchArgs {
     uint16_t* pts;          // [npairs][nb]
     unsigned long long* stats;  // [npairs][3] or null
     uint32_t pcode[8];          // pattern code words (pat_code), see below
+    uint64_t* trace;            // TRACE builds: [npairs][nb][tcap] pass records
+    uint16_t* tlen;             // TRACE builds: [npairs][nb] passes of each block
+    int tcap;
 };
 
 __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
@@ -235,10 +238,22 @@ __device__ __forceinline__ int code_dy(uint32_t w, int k) { return (int)((w >> (
 // ----------------------------------------------------------------------------------------
 // One group pass (all lanes of the warp call it; every group advances its own state).
 // ----------------------------------------------------------------------------------------
-template <int B, int G>
+template <int B, int G, bool TRACE = false>
 struct GroupState {
     static constexpr int R = B / G;   // rows per lane (lane j of a group: rows j, j+G, ...)
     static constexpr int W4 = B / 4;  // 32-bit words per block row
+    // TRACE builds only (me_dcds_trace_batch): one record per scoring pass of the block,
+    // bits 0-7 pass (0 = Step 1), 8-11 pattern row (15 = HCSP), 12-19 slots scored,
+    // 20-27 / 28-35 pattern centre dx / dy (int8), 36-51 incumbent SAD after the pass
+    uint64_t* tr = nullptr;
+    int tcap = 0, npass = 0;
+    __device__ __forceinline__ void trace(int j, int row, unsigned mask, int ccx, int ccy) {
+        if (TRACE && j == 0 && npass < tcap)
+            tr[npass] = (uint64_t)(npass & 0xff) | ((uint64_t)row << 8) | ((uint64_t)(mask & 0xff) << 12) |
+                        ((uint64_t)(ccx & 0xff) << 20) | ((uint64_t)(ccy & 0xff) << 28) |
+                        ((uint64_t)(best & 0xffff) << 36);
+        if (TRACE) npass++;
+    }
     int st = ST_DONE, pid = 0, kind = 0, cx = 0, cy = 0, pts = 0;
     int want = 0;  // slot mask of the next pass (0 when done / idle)
     int bofs = 0, cpos = 0;
@@ -316,6 +331,7 @@ struct GroupState {
         }
         pts = __popc(feas);
         best = key >> 3;
+        trace(j, 15, feas, 0, 0);
         const int kb = key & 7;
         if (kb == 0) {  // halfway stop: finish with no further slots
             st = ST_S4; pid = 4; want = 0;
@@ -408,6 +424,8 @@ struct GroupState {
 
         // ---- advance the state machine (group-uniform)
         bool fin = false;
+        const int ccx = cx, ccy = cy, cpid = pid;
+        const bool scoring = (st == ST_S3 || st == ST_S4);
         if (st != ST_S4PRE) pts += __popc(m4);
         if (st == ST_S3) {
             // Step 2 / Step 3
@@ -435,12 +453,13 @@ struct GroupState {
             }
             fin = true;
         }
+        if (TRACE && scoring) trace(j, cpid, m4, ccx, ccy);
 
         return fin;
     }
 };
 
-template <int B, int G, int NWARP, int VARIANT>
+template <int B, int G, int NWARP, int VARIANT, bool TRACE = false>
 __global__ void __launch_bounds__(NWARP * 32)
     dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
                 const SearchArgs a) {
@@ -498,7 +517,7 @@ __global__ void __launch_bounds__(NWARP * 32)
     const int nbt = tbx_e * tby_e;
     const float inv_tbx = __frcp_rn((float)tbx_e);
 
-    GroupState<B, G> gs;  // group state (every lane of a group holds the same values)
+    GroupState<B, G, TRACE> gs;  // group state (every lane of a group holds the same values)
     long long gblk = 0;
     unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
 
@@ -524,6 +543,7 @@ __global__ void __launch_bounds__(NWARP * 32)
                         const int lbx = idx - lby * tbx_e;
                         const int bxg = x0 + lbx * B, byg = y0 + lby * B;
                         gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
+                        if (TRACE) { gs.tr = a.trace + gblk * a.tcap; gs.tcap = a.tcap; gs.npass = 0; }
                         gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW,
                                  j, bm, a.bm_words);
                     } else {
@@ -552,6 +572,7 @@ __global__ void __launch_bounds__(NWARP * 32)
                     a.mv[gblk] = (uint32_t)(gs.cx & 0xffff) | ((uint32_t)gs.cy << 16);
                     a.sad[gblk] = gs.best;
                     a.pts[gblk] = (uint16_t)gs.pts;
+                    if (TRACE) a.tlen[gblk] = (uint16_t)gs.npass;
                     acc_pts += (unsigned)gs.pts;
                     acc_sad += gs.best;
                     acc_sse += ss;

@@ -188,11 +188,23 @@ int make_tmap(CUtensorMap* tm, const uint8_t* base, int W, int H, int npairs, lo
     return ME_OK;
 }
 
+// Trace builds (me_dcds_trace_batch) exist for the default geometry only.
+template <int B, int G, int NW>
+void launch_dcds_trace(const DcdsLaunch& L, int variant, const CUtensorMap& tc, const CUtensorMap& tr,
+                       cudaStream_t s) {
+    if (variant) me::dcds_kernel<B, G, NW, 1, true><<<L.grid, NW * 32, L.smem, s>>>(tc, tr, L.a);
+    else me::dcds_kernel<B, G, NW, 0, true><<<L.grid, NW * 32, L.smem, s>>>(tc, tr, L.a);
+}
+
 int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W, int H,
              int block, int p, int16_t* mv, uint32_t* sad, uint16_t* pts, uint64_t* stats,
-             int variant, cudaStream_t s) {
+             int variant, cudaStream_t s, uint64_t* trace = nullptr, uint16_t* tlen = nullptr,
+             int tcap = 0) {
     DcdsLaunch L = plan_dcds(W, H, block, p, npairs);
     if ((int)L.smem > g_smem_optin) return fail(ME_EINVAL, "tile does not fit in shared memory");
+    if (trace && !(L.G == (block == 16 ? 8 : 2) && L.NW == (block == 16 ? 8 : 4)))
+        return fail(ME_EINVAL, "trace builds exist for the default lane-group geometry only (unset ME_G/ME_NW)");
+    L.a.trace = trace; L.a.tlen = tlen; L.a.tcap = tcap;
     L.a.cur0 = cur0; L.a.ref0 = ref0; L.a.stride = stride;
     L.a.mv = reinterpret_cast<uint32_t*>(mv);
     L.a.sad = sad;
@@ -204,7 +216,10 @@ int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npa
     rc = make_tmap(&tr, ref0, W, H, npairs, stride, L.a.pitch, L.a.rh);
     if (rc) return rc;
     if (stats) CK(cudaMemsetAsync(stats, 0, sizeof(uint64_t) * 3 * (size_t)npairs, s));
-    if (block == 16) {
+    if (trace) {
+        if (block == 16) launch_dcds_trace<16, 8, 8>(L, variant, tc, tr, s);
+        else launch_dcds_trace<8, 2, 4>(L, variant, tc, tr, s);
+    } else if (block == 16) {
         if (variant) launch_dcds_b<16, 1>(L, tc, tr, s); else launch_dcds_b<16, 0>(L, tc, tr, s);
     } else {
         if (variant) launch_dcds_b<8, 1>(L, tc, tr, s); else launch_dcds_b<8, 0>(L, tc, tr, s);
@@ -398,6 +413,10 @@ int me_init(int device) {
     if ((rc = allow_smem(me::dcds_kernel<B, G, 8, V>))) return rc;
     ME_DCDS_KERNELS(ME_ALLOW)
 #undef ME_ALLOW
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, true>))) return rc;
 #define ME_ALLOW_BMA(B, G, NW)                                                           \
     if ((rc = allow_smem(me::bma_kernel<B, G, NW, me::ALG_CDS>))) return rc;            \
     if ((rc = allow_smem(me::bma_kernel<B, G, NW, me::ALG_DS>))) return rc;             \
@@ -450,6 +469,23 @@ int me_dcds_s_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_strid
     if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
     return run_dcds(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
                     stats_out, 1, g_stream);
+}
+
+int me_dcds_trace_batch(int variant, const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride,
+                        int npairs, int W, int H, int block, int p, int16_t* mv_out,
+                        uint32_t* sad_out, uint16_t* points_out, uint64_t* trace_out, int trace_cap,
+                        uint16_t* trace_len_out) {
+    if (variant != 0 && variant != 1) return fail(ME_EINVAL, "variant must be 0 (DCDS) or 1 (DCDS^S)");
+    int rc = validate_search(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out,
+                             points_out);
+    if (rc) return rc;
+    if (trace_cap < 1 || trace_cap > 255) return fail(ME_EINVAL, "trace_cap must be in [1, 255]");
+    if (!trace_out || !trace_len_out) return fail(ME_EINVAL, "NULL trace pointer");
+    if (!aligned(trace_out, 8) || !aligned(trace_len_out, 2))
+        return fail(ME_EALIGN, "trace_out must be 8-byte aligned, trace_len_out 2-byte");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    return run_dcds(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
+                    nullptr, variant, g_stream, trace_out, trace_len_out, trace_cap);
 }
 
 int me_bma_batch(int alg, const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,

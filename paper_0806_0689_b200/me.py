@@ -21,7 +21,7 @@ SYMBOLS = (
     "me_init", "me_set_stream", "me_dcds", "me_fullsearch", "me_mc_psnr", "me_dcds_batch",
     "me_dcds_s_batch", "me_fullsearch_batch", "me_mc_sse_batch", "me_dcds_batch_host",
     "me_launch_count", "me_strerror", "me_shutdown", "me_quality_batch", "me_bma_batch",
-    "me_ideal_nsp_map", "me_mv_hist",
+    "me_ideal_nsp_map", "me_mv_hist", "me_dcds_trace_batch",
 )
 
 # me_alg ids (include/me.h)
@@ -63,6 +63,7 @@ def load() -> ctypes.CDLL:
     L.me_bma_batch.argtypes = [i32] + batch
     L.me_ideal_nsp_map.argtypes = [i32, i32, vp, vp, vp]
     L.me_mv_hist.argtypes = [vp, i64, i32, vp]
+    L.me_dcds_trace_batch.argtypes = [i32] + batch[:-1] + [vp, i32, vp]
     L.me_launch_count.argtypes = []
     L.me_launch_count.restype = i64
     L.me_strerror.argtypes = [i32]
@@ -168,6 +169,43 @@ def me_bma_batch(alg, frames, block, p, mv, sad, pts, stats=None):
     a = ALGS[alg] if isinstance(alg, str) else int(alg)
     fn = load().me_bma_batch
     _batch(lambda *args: fn(a, *args), frames, block, p, mv, sad, pts, stats)
+
+
+def me_dcds_trace_batch(variant, frames, block, p, mv, sad, pts, trace, trace_len):
+    """DCDS (variant 0) / DCDS^S (1) with a per-pass trace (include/me.h): trace is an int64
+    tensor [npairs, nb, cap] (cap <= 255), trace_len an int16 tensor [npairs, nb]."""
+    if trace.dtype != torch.int64 or trace.dim() != 3 or not trace.is_contiguous():
+        raise ValueError("trace must be a contiguous [npairs, nb, cap] int64 tensor")
+    cap = trace.shape[-1]
+    fn = load().me_dcds_trace_batch
+    _batch(lambda *a: fn(int(variant), *a[:-1], _ptr(trace), cap, _ptr(trace_len)),
+           frames, block, p, mv, sad, pts, None)
+
+
+# slot offsets (dx, dy) of the traced patterns (reading C7; pattern ids of include/me.h)
+_TRACE_SLOTS = {
+    15: ((0, 0), (-1, 0), (1, 0), (-2, 0), (2, 0), (0, -1), (0, 1)),
+    2: ((-2, 0), (2, 0), (0, -1), (0, 1)),
+    3: ((-1, 0), (1, 0), (0, -2), (0, 2)),
+    4: ((-1, 0), (1, 0)),
+    5: ((0, -1), (0, 1)),
+}
+# pattern id -> trace kind (0 HCSP, 1 HDSP, 2 VDSP, 3 middle point)
+_TRACE_KIND = {15: 0, 2: 1, 3: 2, 4: 3, 5: 3}
+
+
+def decode_trace(records, n):
+    """Expand n trace records of one block into the scored points, in scoring order, as
+    (step, dx, dy, kind) tuples (step 0 = Step 1; kind 0 HCSP, 1 HDSP, 2 VDSP, 3 middle)."""
+    out = []
+    for r in [int(x) & 0xFFFFFFFFFFFFFFFF for x in records[:n]]:
+        step, pid, mask = r & 0xFF, (r >> 8) & 0xF, (r >> 12) & 0xFF
+        cx, cy = ((r >> 20) & 0xFF), ((r >> 28) & 0xFF)
+        cx, cy = cx - 256 if cx > 127 else cx, cy - 256 if cy > 127 else cy
+        for k, (ox, oy) in enumerate(_TRACE_SLOTS[pid]):
+            if (mask >> k) & 1:
+                out.append((step, cx + ox, cy + oy, _TRACE_KIND[pid]))
+    return out
 
 
 def me_ideal_nsp_map(alg, p, device="cuda"):
