@@ -41,7 +41,7 @@ struct SearchArgs {
     int pitch, rh;          // staged reference region: row pitch (bytes, 16*odd) and rows
     int cur_off;            // byte offset of the current tile in shared memory (128-aligned)
     int bm_words;           // visited-bitmap words per warp (multiple of 4)
-    int nbx, nb;            // blocks per row, blocks per pair
+    int nbx, nby, nb;       // blocks per row, block rows, blocks per pair
     uint32_t* mv;           // [npairs][nb] packed (dx & 0xffff) | (dy << 16)
     uint32_t* sad;          // [npairs][nb]
     uint16_t* pts;          // [npairs][nb]
@@ -459,7 +459,12 @@ struct GroupState {
     }
 };
 
-template <int B, int G, int NWARP, int VARIANT, bool TRACE = false>
+// ONE: the tile holds at most one block per lane group (the default geometries: 16x4 blocks
+// for 64 groups at B=8, 8x4 for 32 groups at B=16) -- every group takes its block at the
+// start, keeps the finished search in registers, and the SSE and outputs of all blocks are
+// produced in one dense phase after the last search ends.  Otherwise blocks are handed out
+// from a tile counter as groups finish.
+template <int B, int G, int NWARP, int VARIANT, bool TRACE = false, bool ONE = false>
 __global__ void __launch_bounds__(NWARP * 32)
     dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
                 const SearchArgs a) {
@@ -472,8 +477,8 @@ __global__ void __launch_bounds__(NWARP * 32)
     uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = lane % G, g = lane / G, leader = g * G;
-    const int pair = blockIdx.y;
-    const int tx = blockIdx.x % a.ntx, ty = blockIdx.x / a.ntx;
+    const int pair = blockIdx.z;
+    const int tx = blockIdx.x, ty = blockIdx.y;
     const int TW = a.tbx * B, TH = a.tby * B;
     const int x0 = tx * TW, y0 = ty * TH;
     const int xs = (x0 - a.p) & ~15;  // floor to 16 (two's complement)
@@ -512,16 +517,53 @@ __global__ void __launch_bounds__(NWARP * 32)
     const uint32_t* s = reinterpret_cast<const uint32_t*>(sref);
     const int rstride = G * pitch;  // bytes between a lane's rows
     const int jrow = j * pitch;     // byte offset of the lane's first row
-    const int nby = a.nb / a.nbx;
-    const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, nby - ty * a.tby);
+    const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, a.nby - ty * a.tby);
     const int nbt = tbx_e * tby_e;
-    const float inv_tbx = __frcp_rn((float)tbx_e);
 
     GroupState<B, G, TRACE> gs;  // group state (every lane of a group holds the same values)
     long long gblk = 0;
     unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
 
-    for (;;) {
+    // block idx of the tile (row-major over tbx_e columns): start its search
+    auto take = [&](int idx) {
+        const int lby = idx / tbx_e;
+        const int lbx = idx - lby * tbx_e;
+        const int bxg = x0 + lbx * B, byg = y0 + lby * B;
+        gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
+        if (TRACE) { gs.tr = a.trace + gblk * a.tcap; gs.tcap = a.tcap; gs.npass = 0; }
+        gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW, j, bm,
+                 a.bm_words);
+    };
+
+    if constexpr (ONE) {
+        const int idx = warp * NG + g;
+        const bool have = idx < nbt;
+        if (have) take(idx);
+        else { gs.st = ST_IDLE; gs.want = 0; }
+        __syncwarp();
+        if (__any_sync(FULL, have)) {
+            gs.step1(s, bm, j, p, pitch, rstride, jrow);
+            __syncwarp();  // the visited bits are set before the pass tests them
+            while (__any_sync(FULL, gs.st != ST_DONE && gs.st != ST_IDLE))
+                if (gs.template pass<VARIANT>(s, bm, s_pcode, s_poff, j, leader, p, pitch, rstride, jrow)) {
+                    gs.st = ST_DONE; gs.want = 0;
+                }
+            // every search of the warp ended: SSE of the compensated blocks (P:342 aspect 4)
+            // and the outputs, in one dense phase
+            uint32_t ss = have ? gs.sse_rows(s, jrow, rstride) : 0u;
+#pragma unroll
+            for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
+            if (have && j == 0) {
+                a.mv[gblk] = (uint32_t)(gs.cx & 0xffff) | ((uint32_t)gs.cy << 16);
+                a.sad[gblk] = gs.best;
+                a.pts[gblk] = (uint16_t)gs.pts;
+                if (TRACE) a.tlen[gblk] = (uint16_t)gs.npass;
+                acc_pts = (unsigned)gs.pts;
+                acc_sad = gs.best;
+                acc_sse = ss;
+            }
+        }
+    } else for (;;) {
         // ---- groups that are done take the next block of the tile
         const bool need = (gs.st == ST_DONE);
         const unsigned ball = __ballot_sync(FULL, need && j == 0);
@@ -536,19 +578,8 @@ __global__ void __launch_bounds__(NWARP * 32)
                 int idx = base + __popc(ball & ((1u << lane) - 1u));
                 idx = __shfl_sync(FULL, idx, leader);
                 if (need) {
-                    if (idx < nbt) {
-                        // idx / tbx_e by the correctly rounded reciprocal: exact for idx < 2^16,
-                        // tbx_e <= 2^8 (the +0.5 keeps the product 0.5/tbx_e from an integer)
-                        const int lby = (int)(((float)idx + 0.5f) * inv_tbx);
-                        const int lbx = idx - lby * tbx_e;
-                        const int bxg = x0 + lbx * B, byg = y0 + lby * B;
-                        gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
-                        if (TRACE) { gs.tr = a.trace + gblk * a.tcap; gs.tcap = a.tcap; gs.npass = 0; }
-                        gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW,
-                                 j, bm, a.bm_words);
-                    } else {
-                        gs.st = ST_IDLE; gs.want = 0;
-                    }
+                    if (idx < nbt) take(idx);
+                    else { gs.st = ST_IDLE; gs.want = 0; }
                 }
             }
             __syncwarp();

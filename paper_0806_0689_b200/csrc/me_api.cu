@@ -94,6 +94,7 @@ struct DcdsLaunch {
     int G;
     int NW;  // warps per CTA
     int TW, TH;
+    bool one;  // at most one block per lane group: the ONE kernels (default geometry)
 };
 
 // Launch geometry: lane-group size G, tile of tbx x tby blocks.
@@ -139,18 +140,28 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     const int side = 2 * p + 1;
     a.bm_words = (((side * side + 31) / 32) + 3) & ~3;
     a.nbx = nbx;
+    a.nby = nby;
     a.nb = nbx * nby;
-    L.grid = dim3(a.ntx * nty, npairs);
+    L.grid = dim3(a.ntx, nty, npairs);
     for (int i = 0; i < 8; i++) a.pcode[i] = me::pat_code(i);
     const int groups = L.NW * 32 / L.G;
     a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;  // TMA destinations are 128-byte aligned
     L.TW = TW; L.TH = TH;
+    L.one = tbx * tby <= groups;
     L.smem = 128 + (size_t)a.cur_off + (size_t)TW * TH + (size_t)groups * a.bm_words * 4 + 32;
+    if (const char* e = getenv("ME_SMEM_PAD")) L.smem += (size_t)std::max(0, atoi(e));  // tuning only
     return L;
 }
 
 template <int B, int G, int VARIANT>
 void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap& tr, cudaStream_t s) {
+    constexpr int DG = B == 16 ? 8 : 2, DNW = B == 16 ? 8 : 4;  // default geometry
+    if constexpr (G == DG) {
+        if (L.NW == DNW && L.one) {
+            me::dcds_kernel<B, G, DNW, VARIANT, false, true><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
+            return;
+        }
+    }
     if (L.NW == 2) me::dcds_kernel<B, G, 2, VARIANT><<<L.grid, 64, L.smem, s>>>(tc, tr, L.a);
     else if (L.NW == 8) me::dcds_kernel<B, G, 8, VARIANT><<<L.grid, 256, L.smem, s>>>(tc, tr, L.a);
     else me::dcds_kernel<B, G, 4, VARIANT><<<L.grid, 128, L.smem, s>>>(tc, tr, L.a);
@@ -192,8 +203,13 @@ int make_tmap(CUtensorMap* tm, const uint8_t* base, int W, int H, int npairs, lo
 template <int B, int G, int NW>
 void launch_dcds_trace(const DcdsLaunch& L, int variant, const CUtensorMap& tc, const CUtensorMap& tr,
                        cudaStream_t s) {
-    if (variant) me::dcds_kernel<B, G, NW, 1, true><<<L.grid, NW * 32, L.smem, s>>>(tc, tr, L.a);
-    else me::dcds_kernel<B, G, NW, 0, true><<<L.grid, NW * 32, L.smem, s>>>(tc, tr, L.a);
+    if (L.one) {
+        if (variant) me::dcds_kernel<B, G, NW, 1, true, true><<<L.grid, NW * 32, L.smem, s>>>(tc, tr, L.a);
+        else me::dcds_kernel<B, G, NW, 0, true, true><<<L.grid, NW * 32, L.smem, s>>>(tc, tr, L.a);
+    } else {
+        if (variant) me::dcds_kernel<B, G, NW, 1, true><<<L.grid, NW * 32, L.smem, s>>>(tc, tr, L.a);
+        else me::dcds_kernel<B, G, NW, 0, true><<<L.grid, NW * 32, L.smem, s>>>(tc, tr, L.a);
+    }
 }
 
 int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W, int H,
@@ -413,6 +429,14 @@ int me_init(int device) {
     if ((rc = allow_smem(me::dcds_kernel<B, G, 8, V>))) return rc;
     ME_DCDS_KERNELS(ME_ALLOW)
 #undef ME_ALLOW
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, false, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, false, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, true, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, true, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, true, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, true, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, true>))) return rc;

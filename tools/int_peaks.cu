@@ -41,6 +41,13 @@ __global__ void kern(uint32_t* out, int iters, uint32_t seed, long long* cycles)
             if (OP == 1) acc[k] = __dp4a(a + k, b, acc[k]);              // IDP.4A
             if (OP == 2) acc[k] = acc[k] + (a ^ k) + b;                  // IADD3
             if (OP == 3) acc[k] = __funnelshift_r(acc[k], b, a + k);     // SHF
+            if (OP == 4) acc[k] = __byte_perm(acc[k], b, a + k);         // PRMT
+            if (OP == 5) acc[k] = k < NCHAIN / 2 ? vsad4(a + k, b, acc[k])    // half VABSDIFF4,
+                                                 : __byte_perm(acc[k], b, a + k);  // half PRMT
+            if (OP == 6) acc[k] = k < NCHAIN / 2 ? vsad4(a + k, b, acc[k])    // half VABSDIFF4,
+                                                 : __funnelshift_r(acc[k], b, a + k);  // half SHF
+            if (OP == 7) acc[k] = k < NCHAIN / 2 ? vsad4(a + k, b, acc[k])    // half VABSDIFF4,
+                                                 : acc[k] + (a ^ k) + b;   // half IADD3/LOP3
         }
     }
     long long t1 = clock64();
@@ -96,6 +103,10 @@ int main() {
     run<1>("dp4a", sms, 8, 256, 200000, &r);
     run<2>("iadd3", sms, 8, 256, 200000, &r);
     run<3>("shf", sms, 8, 256, 200000, &r);
+    run<4>("prmt", sms, 8, 256, 200000, &r);
+    run<5>("vabsdiff4_prmt_mix", sms, 8, 256, 200000, &r);
+    run<6>("vabsdiff4_shf_mix", sms, 8, 256, 200000, &r);
+    run<7>("vabsdiff4_iadd_mix", sms, 8, 256, 200000, &r);
     printf("  \"nchain\": %d, \"threads_per_sm\": %d\n}\n", NCHAIN, 8 * 256);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
