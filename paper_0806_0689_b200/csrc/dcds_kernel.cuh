@@ -40,7 +40,8 @@ struct SearchArgs {
     int tbx, tby, ntx;      // tile size in blocks; tiles per row
     int pitch, rh;          // staged reference region: row pitch (bytes, 16*odd) and rows
     int cur_off;            // byte offset of the current tile in shared memory (128-aligned)
-    int bm_words;           // visited-bitmap words per warp (multiple of 4)
+    int bm_off, init_off;   // byte offsets of the group bitmaps and of the bitmap template
+    int bm_words;           // visited-bitmap words per group (bm_nwords(p))
     int nbx, nby, nb;       // blocks per row, block rows, blocks per pair
     uint32_t* mv;           // [npairs][nb] packed (dx & 0xffff) | (dy << 16)
     uint32_t* sad;          // [npairs][nb]
@@ -180,16 +181,6 @@ __device__ __forceinline__ uint32_t sad_shift(const uint32_t (&c)[W4], const uin
     return acc;
 }
 
-// Offsets of the DDSP points in the fixed order (reading C7), candidate k = 0..3.
-//   HDSP: (-2,0) (2,0) (0,-1) (0,1)      VDSP: (-1,0) (1,0) (0,-2) (0,2)
-__device__ __forceinline__ int ddsp_dx(int kind, int k) {
-    return kind == 0 ? (k < 2 ? 4 * k - 2 : 0) : (k < 2 ? 2 * k - 1 : 0);
-}
-__device__ __forceinline__ int ddsp_dy(int kind, int k) {
-    return kind == 0 ? (k < 2 ? 0 : 2 * k - 5) : (k < 2 ? 0 : 4 * k - 10);
-}
-// near point of the pattern (L1 distance 1): HDSP k >= 2, VDSP k < 2.
-__device__ __forceinline__ bool ddsp_near(int kind, int k) { return kind == 0 ? k >= 2 : k < 2; }
 // HCSP order: (0,0) (-1,0) (1,0) (-2,0) (2,0) (0,-1) (0,1), k = 0..6
 __device__ __forceinline__ int hcsp_dx(int k) {
     return k == 0 ? 0 : (k <= 4 ? ((k & 1) ? -((k + 1) >> 1) : (k >> 1)) : 0);
@@ -200,34 +191,38 @@ __device__ __forceinline__ int hcsp_dy(int k) { return k < 5 ? 0 : (k == 5 ? -1 
 // Lane-group state machine.
 //
 // Each pass evaluates the (up to) 4 candidate slots of one search pattern, given by a
-// pattern id:  0 S1A  HCSP points (0,0) (-1,0) (1,0) (-2,0)       [Step 1, first half]
-//              1 S1B  HCSP points (2,0) (0,-1) (0,1)               [Step 1, second half]
-//              2 S3H  HDSP (-2,0) (2,0) (0,-1) (0,1)               [Steps 2-3, P:257]
+// pattern id:  2 S3H  HDSP (-2,0) (2,0) (0,-1) (0,1)               [Steps 2-3, P:257]
 //              3 S3V  VDSP (-1,0) (1,0) (0,-2) (0,2)
 //              4 S4H  middle points (-1,0) (1,0)                    [Step 4]
 //              5 S4V  middle points (0,-1) (0,1)
 //              6 PREH distant points (-2,0) (2,0)   (DCDS^S look-up, not counted)
 //              7 PREV distant points (0,-2) (0,2)
-// Slot order is the fixed pattern order of reading C7.  A table in shared memory holds, per
-// pattern, the byte offset of every slot in the staged region (dy*pitch + dx) and a packed
-// code word: bits 6k..6k+5 = (dx+2) | (dy+2) << 3 of slot k, bits 24..27 = slots in use.
+// (ids 0 / 1 name the two halves of the HCSP in the trace format; Step 1 itself runs as one
+// straight-line step, GroupState::step1.)  Slot order is the fixed pattern order of reading
+// C7.  Two tables in shared memory hold, per pattern, every slot's byte offset in the staged
+// region (dy*pitch + dx) and its offset in the visited bitmap (dy*BW + dx, below).
+//
+// Visited bitmap (reading C5) of a group: one bit per candidate of the +-p window plus a
+// 2-wide border, row length BW = 2p+3 (the 2 border columns between consecutive rows serve
+// as the right border of one row and the left border of the next): bit of (dx, dy) =
+// (dy+p+2)*BW + (dx+p+2).  The border bits start set, so a pattern point outside the window
+// (reading C8; pattern offsets are at most 2) reads as "already visited" and is neither
+// scored nor counted -- the test-and-set is the whole feasibility test.
 // ----------------------------------------------------------------------------------------
 enum : int { ST_DONE = 0, ST_S1A = 1, ST_S1B = 2, ST_S3 = 3, ST_S4 = 4, ST_S4PRE = 5, ST_IDLE = 6 };
 
-// Pattern table (dx, dy per slot) -- the code words are built once per launch.
+// Pattern table (dx, dy per slot), ids as above.
 struct PatTable {
     int d[8][4][2];
-    uint32_t used[8];
 };
 constexpr PatTable kPat = {
     {{{0, 0}, {-1, 0}, {1, 0}, {-2, 0}}, {{2, 0}, {0, -1}, {0, 1}, {0, 0}},
      {{-2, 0}, {2, 0}, {0, -1}, {0, 1}}, {{-1, 0}, {1, 0}, {0, -2}, {0, 2}},
      {{-1, 0}, {1, 0}, {0, 0}, {0, 0}},  {{0, -1}, {0, 1}, {0, 0}, {0, 0}},
-     {{-2, 0}, {2, 0}, {0, 0}, {0, 0}},  {{0, -2}, {0, 2}, {0, 0}, {0, 0}}},
-    {0xf, 0x7, 0xf, 0xf, 0x3, 0x3, 0x3, 0x3}};
+     {{-2, 0}, {2, 0}, {0, 0}, {0, 0}},  {{0, -2}, {0, 2}, {0, 0}, {0, 0}}}};
 
-inline constexpr uint32_t pat_code(int pid) {  // host side (kernel args)
-    uint32_t w = kPat.used[pid] << 24;
+inline constexpr uint32_t pat_code(int pid) {  // host side (kernel args): 6 bits per slot
+    uint32_t w = 0;
     for (int k = 0; k < 4; k++)
         w |= (uint32_t)((kPat.d[pid][k][0] + 2) | ((kPat.d[pid][k][1] + 2) << 3)) << (6 * k);
     return w;
@@ -235,13 +230,24 @@ inline constexpr uint32_t pat_code(int pid) {  // host side (kernel args)
 __device__ __forceinline__ int code_dx(uint32_t w, int k) { return (int)((w >> (6 * k)) & 7u) - 2; }
 __device__ __forceinline__ int code_dy(uint32_t w, int k) { return (int)((w >> (6 * k + 3)) & 7u) - 2; }
 
-// ----------------------------------------------------------------------------------------
-// One group pass (all lanes of the warp call it; every group advances its own state).
-// ----------------------------------------------------------------------------------------
+// Visited-bitmap geometry for window +-p: row length, words (even, for 8-byte copies).
+__host__ __device__ constexpr int bm_row(int p) { return 2 * p + 3; }
+__host__ __device__ constexpr int bm_nwords(int p) {
+    return ((((2 * p + 5) * bm_row(p) + 2 + 31) / 32) + 1) & ~1;
+}
+
+__device__ __forceinline__ int pick4(const int4& v, int k) {
+    return (k & 2) ? ((k & 1) ? v.w : v.z) : ((k & 1) ? v.y : v.x);
+}
+
 template <int B, int G, bool TRACE = false>
 struct GroupState {
     static constexpr int R = B / G;   // rows per lane (lane j of a group: rows j, j+G, ...)
     static constexpr int W4 = B / 4;  // 32-bit words per block row
+    // 8x8 blocks: a slot with no new point gets the sum SENT (> any SAD, 255*64 = 16320) so
+    // the argmin needs no mask; 16x16 SADs (<= 65280) leave no room in the 16-bit fields.
+    static constexpr bool SENTINEL = (B == 8);
+    static constexpr uint32_t SENT_LANE = 16384u / G;
     // TRACE builds only (me_dcds_trace_batch): one record per scoring pass of the block,
     // bits 0-7 pass (0 = Step 1), 8-11 pattern row (15 = HCSP), 12-19 slots scored,
     // 20-27 / 28-35 pattern centre dx / dy (int8), 36-51 incumbent SAD after the pass
@@ -254,17 +260,23 @@ struct GroupState {
                         ((uint64_t)(best & 0xffff) << 36);
         if (TRACE) npass++;
     }
-    int st = ST_DONE, pid = 0, kind = 0, cx = 0, cy = 0, pts = 0;
+    int st = ST_DONE, pid = 0, kind = 0, pts = 0;
     int want = 0;  // slot mask of the next pass (0 when done / idle)
-    int bofs = 0, cpos = 0;
+    int bofs = 0, cpos = 0;  // staged byte offset of the (0,0) candidate / of the centre
+    int cidx = 0;            // visited-bitmap bit of the centre
     uint32_t best = 0;
     uint32_t cw[R][W4];
 
-    // Start the search of the block whose (0,0) candidate is at byte `origin` of the staged
-    // region and whose current rows are at `crow0` (row stride `cpitch`): load the lane's
-    // current rows, clear the group's visited bitmap (reading C5), enter Step 1.
-    __device__ __forceinline__ void start(int origin, const uint8_t* crow0, int cpitch, int j,
-                                          uint32_t* bm, int bm_words) {
+    // centre (dx, dy) from its bitmap bit (the row length exceeds 2p + 1)
+    __device__ __forceinline__ void centre(int p, int& cx, int& cy) const {
+        const int bw = bm_row(p);
+        const int row = cidx / bw;
+        cy = row - p - 2;
+        cx = cidx - row * bw - p - 2;
+    }
+
+    // Load the lane's current rows of the block at `crow0` (row stride `cpitch`).
+    __device__ __forceinline__ void load_cur(int origin, const uint8_t* crow0, int cpitch, int j) {
         bofs = origin;
         cpos = origin;
 #pragma unroll
@@ -273,10 +285,16 @@ struct GroupState {
 #pragma unroll
             for (int w = 0; w < W4; w++) cw[r][w] = crow[w];
         }
+    }
+    // Reset the group's visited bitmap to the border template and enter Step 1.
+    __device__ __forceinline__ void init_search(int j, uint32_t* bm, const uint32_t* bm_init,
+                                                int bm_words, int p) {
 #pragma unroll 4
-        for (int w = j * 4; w < bm_words; w += 4 * G)
-            *reinterpret_cast<uint4*>(bm + w) = make_uint4(0, 0, 0, 0);
-        st = ST_S1A; pid = 0; kind = 0; cx = 0; cy = 0; pts = 0; want = 0xf;
+        for (int w = j * 2; w < bm_words; w += 2 * G)
+            *reinterpret_cast<uint2*>(bm + w) = *reinterpret_cast<const uint2*>(bm_init + w);
+        const int bw = bm_row(p);
+        cidx = (p + 2) * bw + p + 2;
+        st = ST_S1A; pid = 0; kind = 0; pts = 0; want = 0xf;
     }
 
     // Step 1 of a block that starts it now (st == ST_S1A), in one straight-line
@@ -322,9 +340,10 @@ struct GroupState {
             if ((feas >> k) & 1) key = min(key, (sad << 3) | k);
         }
         // visited set (reading C5): the group's first lane marks the scored points
+        const int bw = bm_row(p);
         if (j == 0) {
-            const int side = 2 * p + 1, c = p * side + p;
-            const int idx[7] = {c, c - 1, c + 1, c - 2, c + 2, c - side, c + side};
+            const int c = cidx;
+            const int idx[7] = {c, c - 1, c + 1, c - 2, c + 2, c - bw, c + bw};
 #pragma unroll
             for (int k = 0; k < 7; k++)
                 if ((feas >> k) & 1) bm[idx[k] >> 5] |= 1u << (idx[k] & 31);
@@ -336,9 +355,9 @@ struct GroupState {
         if (kb == 0) {  // halfway stop: finish with no further slots
             st = ST_S4; pid = 4; want = 0;
         } else {
-            cx = hcsp_dx(kb);
-            cy = hcsp_dy(kb);
+            const int cx = hcsp_dx(kb), cy = hcsp_dy(kb);
             cpos = bofs + cy * pitch + cx;
+            cidx += cy * bw + cx;
             kind = (cy == 0) ? 0 : 1;  // switching strategy one
             st = ST_S3; pid = 2 + kind; want = 0xf;
         }
@@ -357,13 +376,13 @@ struct GroupState {
     }
 
     // One pass of the group's state machine; returns true when the block's search ended.
+    // s_poff / s_pbit: per-pattern slot offsets (bytes / bitmap bits); bm_init: the border
+    // template (the DCDS^S look-up's window test).
     template <int VARIANT>
-    __device__ __forceinline__ bool pass(const uint32_t* s, uint32_t* bm, const uint32_t* s_pcode,
-                                         const int4* s_poff, int j, int leader, int p, int pitch,
-                                         int rstride, int jrow) {
-        const uint32_t pw = s_pcode[pid];
-        const int4 po = s_poff[pid];
-        const uint32_t used = (pw >> 24) & (uint32_t)want;
+    __device__ __forceinline__ bool pass(const uint32_t* s, uint32_t* bm, const uint32_t* bm_init,
+                                         const int4* s_poff, const int4* s_pbit, int j, int leader,
+                                         int p, int jrow, int rstride) {
+        const int4 pb = s_pbit[pid];
 
         // ---- visited-set test-and-set (reading C5): lane j of a group owns slots j, j+G, ...
         unsigned m4 = 0;
@@ -371,32 +390,29 @@ struct GroupState {
         for (int h = 0; h < (G >= 4 ? 1 : 4 / G); h++) {
             const int k = j + h * G;
             bool nw = false;
-            if (k < 4 && ((used >> k) & 1)) {
-                const int qx = cx + code_dx(pw, k), qy = cy + code_dy(pw, k);
-                if ((unsigned)(qx + p) <= (unsigned)(2 * p) &&
-                    (unsigned)(qy + p) <= (unsigned)(2 * p)) {  // window only (reading C8)
-                    if (st == ST_S4PRE) {
-                        nw = true;  // DCDS^S look-up of the distant points: not scored again
-                    } else {
-                        const int idx = (qy + p) * (2 * p + 1) + (qx + p);
-                        const uint32_t bit = 1u << (idx & 31);
-                        nw = (atomicOr(&bm[idx >> 5], bit) & bit) == 0;
-                    }
-                }
+            if (k < 4 && ((want >> k) & 1)) {
+                const int idx = cidx + pick4(pb, k);
+                const uint32_t bit = 1u << (idx & 31);
+                if (VARIANT && st == ST_S4PRE)
+                    nw = (bm_init[idx >> 5] & bit) == 0;  // DCDS^S look-up: in the window
+                else
+                    nw = (atomicOr(&bm[idx >> 5], bit) & bit) == 0;
             }
             const unsigned bb = __ballot_sync(FULL, nw) >> leader;
             m4 |= (G >= 4 ? (bb & 0xfu) : ((bb & ((1u << G) - 1u)) << (h * G)));
         }
 
         // ---- SADs of the 4 slots over this lane's rows, packed and reduced over the group
-        const int ok[4] = {po.x, po.y, po.z, po.w};
+        const int4 po = s_poff[pid];
+        const int o = cpos + jrow;
         uint32_t sadk[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            uint32_t acc = 0;
+            uint32_t acc = SENTINEL ? SENT_LANE : 0u;
             if ((m4 >> k) & 1) {  // slots not scored this pass issue no shared-memory loads
                 uint32_t rw[R][W4];
-                ref_rows<R, W4>(s, cpos + ok[k] + jrow, rstride, rw);
+                ref_rows<R, W4>(s, o + pick4(po, k), rstride, rw);
+                acc = 0;
 #pragma unroll
                 for (int r = 0; r < R; r++)
 #pragma unroll
@@ -406,32 +422,37 @@ struct GroupState {
         }
         uint32_t v01 = sadk[0] | (sadk[1] << 16), v23 = sadk[2] | (sadk[3] << 16);
 #pragma unroll
-        for (int o = 1; o < G; o <<= 1) {
-            v01 += __shfl_xor_sync(FULL, v01, o);
-            v23 += __shfl_xor_sync(FULL, v23, o);
+        for (int q = 1; q < G; q <<= 1) {
+            v01 += __shfl_xor_sync(FULL, v01, q);
+            v23 += __shfl_xor_sync(FULL, v23, q);
         }
-        sadk[0] = v01 & 0xffffu; sadk[1] = v01 >> 16;
-        sadk[2] = v23 & 0xffffu; sadk[3] = v23 >> 16;
 
         // ---- argmin over the new points of this pass, (SAD, slot) keys (reading C6/C7)
-        uint32_t key = 0xffffffffu;
+        uint32_t key;
+        if constexpr (SENTINEL) {
+            key = min(min(((v01 & 0xffffu) << 2) | 0u, ((v01 >> 16) << 2) | 1u),
+                      min(((v23 & 0xffffu) << 2) | 2u, ((v23 >> 16) << 2) | 3u));
+        } else {
+            key = 0xffffffffu;
+            const uint32_t sv[4] = {v01 & 0xffffu, v01 >> 16, v23 & 0xffffu, v23 >> 16};
 #pragma unroll
-        for (int k = 0; k < 4; k++)
-            if ((m4 >> k) & 1) key = min(key, (sadk[k] << 2) | k);
+            for (int k = 0; k < 4; k++)
+                if ((m4 >> k) & 1) key = min(key, (sv[k] << 2) | k);
+        }
         const int kb = key & 3;
-        const int mdx = code_dx(pw, kb), mdy = code_dy(pw, kb);
-        const int mo = mdy * pitch + mdx;
 
         // ---- advance the state machine (group-uniform)
         bool fin = false;
-        const int ccx = cx, ccy = cy, cpid = pid;
+        int ccx = 0, ccy = 0;
+        const int cpid = pid;
         const bool scoring = (st == ST_S3 || st == ST_S4);
+        if (TRACE) centre(p, ccx, ccy);
         if (st != ST_S4PRE) pts += __popc(m4);
         if (st == ST_S3) {
             // Step 2 / Step 3
             if ((key >> 2) < best) {
                 best = key >> 2;
-                cx += mdx; cy += mdy; cpos += mo;
+                cpos += pick4(po, kb); cidx += pick4(pb, kb);
                 if ((kb >= 2) != (kind == 1)) { kind ^= 1; pid ^= 1; }  // near point
             } else {
                 st = VARIANT ? ST_S4PRE : ST_S4;  // BMP at the centre -> Step 4
@@ -441,15 +462,15 @@ struct GroupState {
         } else if (st == ST_S4PRE) {
             // DCDS^S: keep only the middle point beside the cheaper distant point;
             // an infeasible distant point costs +inf, ties go to the negative side (C22)
-            const uint32_t dn = (m4 & 1) ? sadk[0] : 0xffffffffu;
-            const uint32_t dp = (m4 & 2) ? sadk[1] : 0xffffffffu;
+            const uint32_t dn = (m4 & 1) ? (v01 & 0xffffu) : 0xffffffffu;
+            const uint32_t dp = (m4 & 2) ? (v01 >> 16) : 0xffffffffu;
             want = (dp < dn) ? 2 : 1;
             st = ST_S4; pid = 4 + kind;
         } else if (st == ST_S4) {
             // Step 4: strict minimum of the middle points against the centre
             if ((key >> 2) < best) {
                 best = key >> 2;
-                cx += mdx; cy += mdy; cpos += mo;
+                cpos += pick4(po, kb); cidx += pick4(pb, kb);
             }
             fin = true;
         }
@@ -464,15 +485,14 @@ struct GroupState {
 // start, keeps the finished search in registers, and the SSE and outputs of all blocks are
 // produced in one dense phase after the last search ends.  Otherwise blocks are handed out
 // from a tile counter as groups finish.
-template <int B, int G, int NWARP, int VARIANT, bool TRACE = false, bool ONE = false>
+template <int B, int G, int NWARP, int VARIANT, bool TRACE = false, bool ONE = false, int PITCH = 0>
 __global__ void __launch_bounds__(NWARP * 32)
     dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
                 const SearchArgs a) {
     static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "lane-group size");
     constexpr int NG = 32 / G;    // groups per warp (rows per lane and words per row: GroupState)
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    __shared__ int4 s_poff[8];
-    __shared__ uint32_t s_pcode[8];
+    __shared__ int4 s_poff[8], s_pbit[8];
     __shared__ __align__(8) uint64_t s_bar;
     uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -483,14 +503,17 @@ __global__ void __launch_bounds__(NWARP * 32)
     const int x0 = tx * TW, y0 = ty * TH;
     const int xs = (x0 - a.p) & ~15;  // floor to 16 (two's complement)
     const int ys = y0 - a.p;
-    const int pitch = a.pitch, p = a.p;
+    const int pitch = PITCH ? PITCH : a.pitch, p = a.p;
 
-    // shared layout: reference region (pitch x rh) | current tile (TW x TH) | bitmaps | stats
+    // shared layout: reference region (pitch x rh) | current tile (TW x TH) | group bitmaps |
+    // bitmap template | tile counter.  ONE kernels overlay the bitmaps on the current tile,
+    // which is read into registers before the bitmaps are initialised.
     uint8_t* sref = smem;
     uint8_t* scur = smem + a.cur_off;
-    uint32_t* bms = reinterpret_cast<uint32_t*>(scur + TW * TH);
+    uint32_t* bms = reinterpret_cast<uint32_t*>(smem + a.bm_off);
     uint32_t* bm = bms + (warp * NG + g) * a.bm_words;
-    int* ctr = reinterpret_cast<int*>(bms + NWARP * NG * a.bm_words);
+    uint32_t* bm_init = reinterpret_cast<uint32_t*>(smem + a.init_off);
+    int* ctr = reinterpret_cast<int*>(bm_init + a.bm_words);
 
     // ---- stage the tile with TMA: reference region + current tile, one mbarrier
     if (threadIdx.x == 0) mbar_init(&s_bar, 1);
@@ -499,15 +522,29 @@ __global__ void __launch_bounds__(NWARP * 32)
         mbar_expect_tx(&s_bar, (uint32_t)(pitch * a.rh + TW * TH));
         tma_load_3d(sref, &tm_ref, xs, ys, pair, &s_bar);
         tma_load_3d(scur, &tm_cur, x0, y0, pair, &s_bar);
+        *ctr = 0;
     }
-    if (threadIdx.x == 0) *ctr = 0;
+    const int bw = bm_row(p);
     if (threadIdx.x < 8) {
         const uint32_t w = a.pcode[threadIdx.x];
-        s_pcode[threadIdx.x] = w;
         s_poff[threadIdx.x] = make_int4(code_dy(w, 0) * pitch + code_dx(w, 0),
                                         code_dy(w, 1) * pitch + code_dx(w, 1),
                                         code_dy(w, 2) * pitch + code_dx(w, 2),
                                         code_dy(w, 3) * pitch + code_dx(w, 3));
+        s_pbit[threadIdx.x] = make_int4(code_dy(w, 0) * bw + code_dx(w, 0), code_dy(w, 1) * bw + code_dx(w, 1),
+                                        code_dy(w, 2) * bw + code_dx(w, 2), code_dy(w, 3) * bw + code_dx(w, 3));
+    }
+    // bitmap template: border bits set (rows < 2 or >= 2p+3, columns < 2 of the row length)
+    for (int t = threadIdx.x; t < a.bm_words; t += NWARP * 32) {
+        const int lo = 32 * t;
+        // bits [b0, b1) of the word's range [lo, lo + 32)
+        auto span = [lo](int b0, int b1) -> uint32_t {
+            b0 = max(b0, lo); b1 = min(b1, lo + 32);
+            return b1 > b0 ? (uint32_t)(((1ull << (b1 - b0)) - 1ull) << (b0 - lo)) : 0u;
+        };
+        uint32_t w = span(0, 2 * bw) | span((2 * p + 3) * bw, lo + 32);
+        for (int rs = (lo / bw) * bw; rs < lo + 32; rs += bw) w |= span(rs, rs + 2);
+        bm_init[t] = w;
     }
     mbar_wait(&s_bar, 0);
     if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
@@ -524,28 +561,40 @@ __global__ void __launch_bounds__(NWARP * 32)
     long long gblk = 0;
     unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
 
-    // block idx of the tile (row-major over tbx_e columns): start its search
+    // block idx of the tile (row-major over tbx_e columns): its output index and current rows
     auto take = [&](int idx) {
         const int lby = idx / tbx_e;
         const int lbx = idx - lby * tbx_e;
         const int bxg = x0 + lbx * B, byg = y0 + lby * B;
         gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
         if (TRACE) { gs.tr = a.trace + gblk * a.tcap; gs.tcap = a.tcap; gs.npass = 0; }
-        gs.start((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW, j, bm,
-                 a.bm_words);
+        gs.load_cur((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW, j);
+    };
+    auto output = [&](uint32_t ss) {
+        int cx, cy;
+        gs.centre(p, cx, cy);
+        a.mv[gblk] = (uint32_t)(cx & 0xffff) | ((uint32_t)cy << 16);
+        a.sad[gblk] = gs.best;
+        a.pts[gblk] = (uint16_t)gs.pts;
+        if (TRACE) a.tlen[gblk] = (uint16_t)gs.npass;
+        acc_pts += (unsigned)gs.pts;
+        acc_sad += gs.best;
+        acc_sse += ss;
     };
 
     if constexpr (ONE) {
         const int idx = warp * NG + g;
         const bool have = idx < nbt;
         if (have) take(idx);
+        __syncthreads();  // every current row is in registers: the bitmaps may overwrite them
+        if (have) gs.init_search(j, bm, bm_init, a.bm_words, p);
         else { gs.st = ST_IDLE; gs.want = 0; }
         __syncwarp();
         if (__any_sync(FULL, have)) {
             gs.step1(s, bm, j, p, pitch, rstride, jrow);
             __syncwarp();  // the visited bits are set before the pass tests them
             while (__any_sync(FULL, gs.st != ST_DONE && gs.st != ST_IDLE))
-                if (gs.template pass<VARIANT>(s, bm, s_pcode, s_poff, j, leader, p, pitch, rstride, jrow)) {
+                if (gs.template pass<VARIANT>(s, bm, bm_init, s_poff, s_pbit, j, leader, p, jrow, rstride)) {
                     gs.st = ST_DONE; gs.want = 0;
                 }
             // every search of the warp ended: SSE of the compensated blocks (P:342 aspect 4)
@@ -553,15 +602,7 @@ __global__ void __launch_bounds__(NWARP * 32)
             uint32_t ss = have ? gs.sse_rows(s, jrow, rstride) : 0u;
 #pragma unroll
             for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
-            if (have && j == 0) {
-                a.mv[gblk] = (uint32_t)(gs.cx & 0xffff) | ((uint32_t)gs.cy << 16);
-                a.sad[gblk] = gs.best;
-                a.pts[gblk] = (uint16_t)gs.pts;
-                if (TRACE) a.tlen[gblk] = (uint16_t)gs.npass;
-                acc_pts = (unsigned)gs.pts;
-                acc_sad = gs.best;
-                acc_sse = ss;
-            }
+            if (have && j == 0) output(ss);
         }
     } else for (;;) {
         // ---- groups that are done take the next block of the tile
@@ -578,8 +619,12 @@ __global__ void __launch_bounds__(NWARP * 32)
                 int idx = base + __popc(ball & ((1u << lane) - 1u));
                 idx = __shfl_sync(FULL, idx, leader);
                 if (need) {
-                    if (idx < nbt) take(idx);
-                    else { gs.st = ST_IDLE; gs.want = 0; }
+                    if (idx < nbt) {
+                        take(idx);
+                        gs.init_search(j, bm, bm_init, a.bm_words, p);
+                    } else {
+                        gs.st = ST_IDLE; gs.want = 0;
+                    }
                 }
             }
             __syncwarp();
@@ -591,7 +636,7 @@ __global__ void __launch_bounds__(NWARP * 32)
             __syncwarp();  // the visited bits are set before the pass tests them
         }
 
-        const bool fin = gs.template pass<VARIANT>(s, bm, s_pcode, s_poff, j, leader, p, pitch, rstride, jrow);
+        const bool fin = gs.template pass<VARIANT>(s, bm, bm_init, s_poff, s_pbit, j, leader, p, jrow, rstride);
 
         // ---- finished blocks: SSE of the compensated block (P:342 aspect 4), outputs
         if (__any_sync(FULL, fin)) {
@@ -599,15 +644,7 @@ __global__ void __launch_bounds__(NWARP * 32)
 #pragma unroll
             for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
             if (fin) {
-                if (j == 0) {
-                    a.mv[gblk] = (uint32_t)(gs.cx & 0xffff) | ((uint32_t)gs.cy << 16);
-                    a.sad[gblk] = gs.best;
-                    a.pts[gblk] = (uint16_t)gs.pts;
-                    if (TRACE) a.tlen[gblk] = (uint16_t)gs.npass;
-                    acc_pts += (unsigned)gs.pts;
-                    acc_sad += gs.best;
-                    acc_sse += ss;
-                }
+                if (j == 0) output(ss);
                 gs.st = ST_DONE; gs.want = 0;
             }
         }

@@ -137,8 +137,7 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     if (((pitch >> 4) & 1) == 0) pitch += 16;  // 16 * odd bytes: rows spread over the banks
     a.pitch = pitch;
     a.rh = TH + 2 * p;
-    const int side = 2 * p + 1;
-    a.bm_words = (((side * side + 31) / 32) + 3) & ~3;
+    a.bm_words = me::bm_nwords(p);
     a.nbx = nbx;
     a.nby = nby;
     a.nb = nbx * nby;
@@ -147,8 +146,17 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     const int groups = L.NW * 32 / L.G;
     a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;  // TMA destinations are 128-byte aligned
     L.TW = TW; L.TH = TH;
-    L.one = tbx * tby <= groups;
-    L.smem = 128 + (size_t)a.cur_off + (size_t)TW * TH + (size_t)groups * a.bm_words * 4 + 32;
+    // the ONE kernels (one block per lane group) exist for the default geometry
+    L.one = tbx * tby <= groups && L.G == (B == 16 ? 8 : 2) && L.NW == (B == 16 ? 8 : 4);
+    const int bm_bytes = groups * a.bm_words * 4;
+    if (L.one) {  // bitmaps overlay the current tile (read into registers first)
+        a.bm_off = a.cur_off;
+        a.init_off = a.cur_off + ((std::max(TW * TH, bm_bytes) + 15) & ~15);
+    } else {
+        a.bm_off = a.cur_off + TW * TH;
+        a.init_off = a.bm_off + ((bm_bytes + 15) & ~15);
+    }
+    L.smem = 128 + (size_t)a.init_off + (size_t)a.bm_words * 4 + 16;
     if (const char* e = getenv("ME_SMEM_PAD")) L.smem += (size_t)std::max(0, atoi(e));  // tuning only
     return L;
 }
@@ -157,7 +165,7 @@ template <int B, int G, int VARIANT>
 void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap& tr, cudaStream_t s) {
     constexpr int DG = B == 16 ? 8 : 2, DNW = B == 16 ? 8 : 4;  // default geometry
     if constexpr (G == DG) {
-        if (L.NW == DNW && L.one) {
+        if (L.one) {
             me::dcds_kernel<B, G, DNW, VARIANT, false, true><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
             return;
         }
