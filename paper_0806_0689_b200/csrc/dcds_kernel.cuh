@@ -47,7 +47,6 @@ struct SearchArgs {
     uint32_t* sad;          // [npairs][nb]
     uint16_t* pts;          // [npairs][nb]
     unsigned long long* stats;  // [npairs][3] or null
-    uint32_t pcode[8];          // pattern code words (pat_code), see below
     uint64_t* trace;            // TRACE builds: [npairs][nb][tcap] pass records
     uint16_t* tlen;             // TRACE builds: [npairs][nb] passes of each block
     int tcap;
@@ -199,8 +198,9 @@ __device__ __forceinline__ int hcsp_dy(int k) { return k < 5 ? 0 : (k == 5 ? -1 
 //              7 PREV distant points (0,-2) (0,2)
 // (ids 0 / 1 name the two halves of the HCSP in the trace format; Step 1 itself runs as one
 // straight-line step, GroupState::step1.)  Slot order is the fixed pattern order of reading
-// C7.  Two tables in shared memory hold, per pattern, every slot's byte offset in the staged
-// region (dy*pitch + dx) and its offset in the visited bitmap (dy*BW + dx, below).
+// C7: every pattern is -d0, +d0, -d1, +d1, so a group keeps d0 and d1 in registers, as byte
+// offsets in the staged region (dy*pitch + dx) and as offsets in the visited bitmap (dy*BW + dx,
+// below), and updates them when its pattern changes.
 //
 // Visited bitmap (reading C5) of a group: one bit per candidate of the +-p window plus a
 // 2-wide border, row length BW = 2p+3 (the 2 border columns between consecutive rows serve
@@ -211,34 +211,12 @@ __device__ __forceinline__ int hcsp_dy(int k) { return k < 5 ? 0 : (k == 5 ? -1 
 // ----------------------------------------------------------------------------------------
 enum : int { ST_DONE = 0, ST_S1A = 1, ST_S1B = 2, ST_S3 = 3, ST_S4 = 4, ST_S4PRE = 5, ST_IDLE = 6 };
 
-// Pattern table (dx, dy per slot), ids as above.
-struct PatTable {
-    int d[8][4][2];
-};
-constexpr PatTable kPat = {
-    {{{0, 0}, {-1, 0}, {1, 0}, {-2, 0}}, {{2, 0}, {0, -1}, {0, 1}, {0, 0}},
-     {{-2, 0}, {2, 0}, {0, -1}, {0, 1}}, {{-1, 0}, {1, 0}, {0, -2}, {0, 2}},
-     {{-1, 0}, {1, 0}, {0, 0}, {0, 0}},  {{0, -1}, {0, 1}, {0, 0}, {0, 0}},
-     {{-2, 0}, {2, 0}, {0, 0}, {0, 0}},  {{0, -2}, {0, 2}, {0, 0}, {0, 0}}}};
-
-inline constexpr uint32_t pat_code(int pid) {  // host side (kernel args): 6 bits per slot
-    uint32_t w = 0;
-    for (int k = 0; k < 4; k++)
-        w |= (uint32_t)((kPat.d[pid][k][0] + 2) | ((kPat.d[pid][k][1] + 2) << 3)) << (6 * k);
-    return w;
-}
-__device__ __forceinline__ int code_dx(uint32_t w, int k) { return (int)((w >> (6 * k)) & 7u) - 2; }
-__device__ __forceinline__ int code_dy(uint32_t w, int k) { return (int)((w >> (6 * k + 3)) & 7u) - 2; }
-
-// Visited-bitmap geometry for window +-p: row length, words (even, for 8-byte copies).
+// Visited-bitmap geometry for window +-p: row length, words.  The bitmaps of a CTA's groups
+// are interleaved: word w of group gi at bms[w * (groups + 1) + gi], so the groups' test-and-
+// sets spread over the banks and the CTA initialises all bitmaps with dense stores.
 __host__ __device__ constexpr int bm_row(int p) { return 2 * p + 3; }
-__host__ __device__ constexpr int bm_nwords(int p) {
-    return ((((2 * p + 5) * bm_row(p) + 2 + 31) / 32) + 1) & ~1;
-}
+__host__ __device__ constexpr int bm_nwords(int p) { return ((2 * p + 5) * bm_row(p) + 2 + 31) / 32; }
 
-__device__ __forceinline__ int pick4(const int4& v, int k) {
-    return (k & 2) ? ((k & 1) ? v.w : v.z) : ((k & 1) ? v.y : v.x);
-}
 
 template <int B, int G, bool TRACE = false>
 struct GroupState {
@@ -264,8 +242,18 @@ struct GroupState {
     int want = 0;  // slot mask of the next pass (0 when done / idle)
     int bofs = 0, cpos = 0;  // staged byte offset of the (0,0) candidate / of the centre
     int cidx = 0;            // visited-bitmap bit of the centre
+    // the pattern's slots are -d0, +d0, -d1, +d1 (reading C7 order): d0 / d1 as byte offsets in
+    // the staged region (db0, db1) and as bitmap offsets (de0, de1), set on state changes
+    int db0 = 0, db1 = 0, de0 = 0, de1 = 0;
     uint32_t best = 0;
     uint32_t cw[R][W4];
+
+    // move the centre to slot kb of the current pattern
+    __device__ __forceinline__ void move(int kb) {
+        const int db = (kb & 2) ? db1 : db0, de = (kb & 2) ? de1 : de0;
+        cpos += (kb & 1) ? db : -db;
+        cidx += (kb & 1) ? de : -de;
+    }
 
     // centre (dx, dy) from its bitmap bit (the row length exceeds 2p + 1)
     __device__ __forceinline__ void centre(int p, int& cx, int& cy) const {
@@ -273,6 +261,18 @@ struct GroupState {
         const int row = cidx / bw;
         cy = row - p - 2;
         cx = cidx - row * bw - p - 2;
+    }
+
+    // Pattern steps of pid (ids above): HDSP d0 (2,0) d1 (0,1); VDSP (1,0) (0,2); middle points
+    // (1,0) / (0,1); DCDS^S distant points (2,0) / (0,2).
+    __device__ __forceinline__ void set_pattern(int np, int pitch, int bw) {
+        pid = np;
+        const bool v0 = (np == 5 || np == 7);                       // d0 vertical
+        const int a0 = (np == 2 || np == 6 || np == 7) ? 2 : 1;      // |d0|
+        db0 = v0 ? a0 * pitch : a0;
+        de0 = v0 ? a0 * bw : a0;
+        db1 = (np == 3 ? 2 : 1) * pitch;
+        de1 = (np == 3 ? 2 : 1) * bw;
     }
 
     // Load the lane's current rows of the block at `crow0` (row stride `cpitch`).
@@ -286,12 +286,12 @@ struct GroupState {
             for (int w = 0; w < W4; w++) cw[r][w] = crow[w];
         }
     }
-    // Reset the group's visited bitmap to the border template and enter Step 1.
-    __device__ __forceinline__ void init_search(int j, uint32_t* bm, const uint32_t* bm_init,
-                                                int bm_words, int p) {
-#pragma unroll 4
-        for (int w = j * 2; w < bm_words; w += 2 * G)
-            *reinterpret_cast<uint2*>(bm + w) = *reinterpret_cast<const uint2*>(bm_init + w);
+    // Reset the group's visited bitmap (interleaved, word stride bst) to the border template
+    // (skipped when the CTA initialised every bitmap) and enter Step 1.
+    __device__ __forceinline__ void init_search(int j, uint32_t* bm, int bst, const uint32_t* bm_init,
+                                                int bm_words, int p, bool reset) {
+        if (reset)
+            for (int w = j; w < bm_words; w += G) bm[w * bst] = bm_init[w];
         const int bw = bm_row(p);
         cidx = (p + 2) * bw + p + 2;
         st = ST_S1A; pid = 0; kind = 0; pts = 0; want = 0xf;
@@ -304,8 +304,8 @@ struct GroupState {
     // in Step 3 (switching strategy one) or, on the halfway stop, in a Step-4
     // state with no slots, which the next pass finishes.  All lanes of the warp call it (and
     // __syncwarp after it).
-    __device__ __forceinline__ void step1(const uint32_t* s, uint32_t* bm, int j, int p, int pitch,
-                                          int rstride, int jrow) {
+    __device__ __forceinline__ void step1(const uint32_t* s, uint32_t* bm, int bst, int j, int p,
+                                          int pitch, int rstride, int jrow) {
         const bool live = (st == ST_S1A);
         uint32_t sk[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
         if (live) {
@@ -346,7 +346,7 @@ struct GroupState {
             const int idx[7] = {c, c - 1, c + 1, c - 2, c + 2, c - bw, c + bw};
 #pragma unroll
             for (int k = 0; k < 7; k++)
-                if ((feas >> k) & 1) bm[idx[k] >> 5] |= 1u << (idx[k] & 31);
+                if ((feas >> k) & 1) bm[(idx[k] >> 5) * bst] |= 1u << (idx[k] & 31);
         }
         pts = __popc(feas);
         best = key >> 3;
@@ -359,7 +359,8 @@ struct GroupState {
             cpos = bofs + cy * pitch + cx;
             cidx += cy * bw + cx;
             kind = (cy == 0) ? 0 : 1;  // switching strategy one
-            st = ST_S3; pid = 2 + kind; want = 0xf;
+            st = ST_S3; want = 0xf;
+            set_pattern(2 + kind, pitch, bw);
         }
     }
 
@@ -376,14 +377,10 @@ struct GroupState {
     }
 
     // One pass of the group's state machine; returns true when the block's search ended.
-    // s_poff / s_pbit: per-pattern slot offsets (bytes / bitmap bits); bm_init: the border
-    // template (the DCDS^S look-up's window test).
+    // bm_init: the border template (the DCDS^S look-up's window test).
     template <int VARIANT>
-    __device__ __forceinline__ bool pass(const uint32_t* s, uint32_t* bm, const uint32_t* bm_init,
-                                         const int4* s_poff, const int4* s_pbit, int j, int leader,
-                                         int p, int jrow, int rstride) {
-        const int4 pb = s_pbit[pid];
-
+    __device__ __forceinline__ bool pass(const uint32_t* s, uint32_t* bm, int bst, const uint32_t* bm_init,
+                                         int j, int leader, int p, int pitch, int jrow, int rstride) {
         // ---- visited-set test-and-set (reading C5): lane j of a group owns slots j, j+G, ...
         unsigned m4 = 0;
 #pragma unroll
@@ -391,27 +388,28 @@ struct GroupState {
             const int k = j + h * G;
             bool nw = false;
             if (k < 4 && ((want >> k) & 1)) {
-                const int idx = cidx + pick4(pb, k);
+                const int de = (k & 2) ? de1 : de0;
+                const int idx = cidx + ((k & 1) ? de : -de);
                 const uint32_t bit = 1u << (idx & 31);
                 if (VARIANT && st == ST_S4PRE)
                     nw = (bm_init[idx >> 5] & bit) == 0;  // DCDS^S look-up: in the window
                 else
-                    nw = (atomicOr(&bm[idx >> 5], bit) & bit) == 0;
+                    nw = (atomicOr(&bm[(idx >> 5) * bst], bit) & bit) == 0;
             }
             const unsigned bb = __ballot_sync(FULL, nw) >> leader;
             m4 |= (G >= 4 ? (bb & 0xfu) : ((bb & ((1u << G) - 1u)) << (h * G)));
         }
 
         // ---- SADs of the 4 slots over this lane's rows, packed and reduced over the group
-        const int4 po = s_poff[pid];
         const int o = cpos + jrow;
         uint32_t sadk[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             uint32_t acc = SENTINEL ? SENT_LANE : 0u;
             if ((m4 >> k) & 1) {  // slots not scored this pass issue no shared-memory loads
+                const int db = (k & 2) ? db1 : db0;
                 uint32_t rw[R][W4];
-                ref_rows<R, W4>(s, o + pick4(po, k), rstride, rw);
+                ref_rows<R, W4>(s, (k & 1) ? o + db : o - db, rstride, rw);
                 acc = 0;
 #pragma unroll
                 for (int r = 0; r < R; r++)
@@ -452,11 +450,11 @@ struct GroupState {
             // Step 2 / Step 3
             if ((key >> 2) < best) {
                 best = key >> 2;
-                cpos += pick4(po, kb); cidx += pick4(pb, kb);
-                if ((kb >= 2) != (kind == 1)) { kind ^= 1; pid ^= 1; }  // near point
+                move(kb);
+                if ((kb >= 2) != (kind == 1)) { kind ^= 1; set_pattern(pid ^ 1, pitch, bm_row(p)); }  // near point
             } else {
                 st = VARIANT ? ST_S4PRE : ST_S4;  // BMP at the centre -> Step 4
-                pid = (VARIANT ? 6 : 4) + kind;
+                set_pattern((VARIANT ? 6 : 4) + kind, pitch, bm_row(p));
                 want = 3;
             }
         } else if (st == ST_S4PRE) {
@@ -465,12 +463,13 @@ struct GroupState {
             const uint32_t dn = (m4 & 1) ? (v01 & 0xffffu) : 0xffffffffu;
             const uint32_t dp = (m4 & 2) ? (v01 >> 16) : 0xffffffffu;
             want = (dp < dn) ? 2 : 1;
-            st = ST_S4; pid = 4 + kind;
+            st = ST_S4;
+            set_pattern(4 + kind, pitch, bm_row(p));
         } else if (st == ST_S4) {
             // Step 4: strict minimum of the middle points against the centre
             if ((key >> 2) < best) {
                 best = key >> 2;
-                cpos += pick4(po, kb); cidx += pick4(pb, kb);
+                move(kb);
             }
             fin = true;
         }
@@ -486,13 +485,12 @@ struct GroupState {
 // produced in one dense phase after the last search ends.  Otherwise blocks are handed out
 // from a tile counter as groups finish.
 template <int B, int G, int NWARP, int VARIANT, bool TRACE = false, bool ONE = false, int PITCH = 0>
-__global__ void __launch_bounds__(NWARP * 32)
+__global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
     dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
                 const SearchArgs a) {
     static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "lane-group size");
     constexpr int NG = 32 / G;    // groups per warp (rows per lane and words per row: GroupState)
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    __shared__ int4 s_poff[8], s_pbit[8];
     __shared__ __align__(8) uint64_t s_bar;
     uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -511,7 +509,8 @@ __global__ void __launch_bounds__(NWARP * 32)
     uint8_t* sref = smem;
     uint8_t* scur = smem + a.cur_off;
     uint32_t* bms = reinterpret_cast<uint32_t*>(smem + a.bm_off);
-    uint32_t* bm = bms + (warp * NG + g) * a.bm_words;
+    constexpr int BST = NWARP * NG + 1;  // interleaved bitmap word stride
+    uint32_t* bm = bms + (warp * NG + g);
     uint32_t* bm_init = reinterpret_cast<uint32_t*>(smem + a.init_off);
     int* ctr = reinterpret_cast<int*>(bm_init + a.bm_words);
 
@@ -525,15 +524,6 @@ __global__ void __launch_bounds__(NWARP * 32)
         *ctr = 0;
     }
     const int bw = bm_row(p);
-    if (threadIdx.x < 8) {
-        const uint32_t w = a.pcode[threadIdx.x];
-        s_poff[threadIdx.x] = make_int4(code_dy(w, 0) * pitch + code_dx(w, 0),
-                                        code_dy(w, 1) * pitch + code_dx(w, 1),
-                                        code_dy(w, 2) * pitch + code_dx(w, 2),
-                                        code_dy(w, 3) * pitch + code_dx(w, 3));
-        s_pbit[threadIdx.x] = make_int4(code_dy(w, 0) * bw + code_dx(w, 0), code_dy(w, 1) * bw + code_dx(w, 1),
-                                        code_dy(w, 2) * bw + code_dx(w, 2), code_dy(w, 3) * bw + code_dx(w, 3));
-    }
     // bitmap template: border bits set (rows < 2 or >= 2p+3, columns < 2 of the row length)
     for (int t = threadIdx.x; t < a.bm_words; t += NWARP * 32) {
         const int lo = 32 * t;
@@ -587,14 +577,19 @@ __global__ void __launch_bounds__(NWARP * 32)
         const bool have = idx < nbt;
         if (have) take(idx);
         __syncthreads();  // every current row is in registers: the bitmaps may overwrite them
-        if (have) gs.init_search(j, bm, bm_init, a.bm_words, p);
+        // all bitmaps of the CTA at once: word w of every group, dense stores
+        for (int e = threadIdx.x; e < a.bm_words * BST; e += NWARP * 32) {
+            const int w = e / BST;  // constant divisor
+            bms[e] = bm_init[w];
+        }
+        __syncthreads();
+        if (have) gs.init_search(j, bm, BST, bm_init, a.bm_words, p, false);
         else { gs.st = ST_IDLE; gs.want = 0; }
-        __syncwarp();
         if (__any_sync(FULL, have)) {
-            gs.step1(s, bm, j, p, pitch, rstride, jrow);
+            gs.step1(s, bm, BST, j, p, pitch, rstride, jrow);
             __syncwarp();  // the visited bits are set before the pass tests them
             while (__any_sync(FULL, gs.st != ST_DONE && gs.st != ST_IDLE))
-                if (gs.template pass<VARIANT>(s, bm, bm_init, s_poff, s_pbit, j, leader, p, jrow, rstride)) {
+                if (gs.template pass<VARIANT>(s, bm, BST, bm_init, j, leader, p, pitch, jrow, rstride)) {
                     gs.st = ST_DONE; gs.want = 0;
                 }
             // every search of the warp ended: SSE of the compensated blocks (P:342 aspect 4)
@@ -621,7 +616,7 @@ __global__ void __launch_bounds__(NWARP * 32)
                 if (need) {
                     if (idx < nbt) {
                         take(idx);
-                        gs.init_search(j, bm, bm_init, a.bm_words, p);
+                        gs.init_search(j, bm, BST, bm_init, a.bm_words, p, true);
                     } else {
                         gs.st = ST_IDLE; gs.want = 0;
                     }
@@ -632,11 +627,11 @@ __global__ void __launch_bounds__(NWARP * 32)
         if (__all_sync(FULL, gs.st == ST_IDLE)) break;
         // ---- groups that just took a block run Step 1 in one straight-line step
         if (__any_sync(FULL, gs.st == ST_S1A)) {
-            gs.step1(s, bm, j, p, pitch, rstride, jrow);
+            gs.step1(s, bm, BST, j, p, pitch, rstride, jrow);
             __syncwarp();  // the visited bits are set before the pass tests them
         }
 
-        const bool fin = gs.template pass<VARIANT>(s, bm, bm_init, s_poff, s_pbit, j, leader, p, jrow, rstride);
+        const bool fin = gs.template pass<VARIANT>(s, bm, BST, bm_init, j, leader, p, pitch, jrow, rstride);
 
         // ---- finished blocks: SSE of the compensated block (P:342 aspect 4), outputs
         if (__any_sync(FULL, fin)) {

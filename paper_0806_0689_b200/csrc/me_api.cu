@@ -142,13 +142,12 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     a.nby = nby;
     a.nb = nbx * nby;
     L.grid = dim3(a.ntx, nty, npairs);
-    for (int i = 0; i < 8; i++) a.pcode[i] = me::pat_code(i);
     const int groups = L.NW * 32 / L.G;
     a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;  // TMA destinations are 128-byte aligned
     L.TW = TW; L.TH = TH;
     // the ONE kernels (one block per lane group) exist for the default geometry
     L.one = tbx * tby <= groups && L.G == (B == 16 ? 8 : 2) && L.NW == (B == 16 ? 8 : 4);
-    const int bm_bytes = groups * a.bm_words * 4;
+    const int bm_bytes = (groups + 1) * a.bm_words * 4;  // interleaved, word stride groups + 1
     if (L.one) {  // bitmaps overlay the current tile (read into registers first)
         a.bm_off = a.cur_off;
         a.init_off = a.cur_off + ((std::max(TW * TH, bm_bytes) + 15) & ~15);
