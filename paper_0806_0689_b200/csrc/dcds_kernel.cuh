@@ -212,7 +212,7 @@ __device__ __forceinline__ int hcsp_dy(int k) { return k < 5 ? 0 : (k == 5 ? -1 
 enum : int { ST_DONE = 0, ST_S1A = 1, ST_S1B = 2, ST_S3 = 3, ST_S4 = 4, ST_S4PRE = 5, ST_IDLE = 6 };
 
 // Visited-bitmap geometry for window +-p: row length, words.  The bitmaps of a CTA's groups
-// are interleaved: word w of group gi at bms[w * (groups + 1) + gi], so the groups' test-and-
+// are interleaved: word w of group gi at bms[w * (groups + 4) + gi], so the groups' test-and-
 // sets spread over the banks and the CTA initialises all bitmaps with dense stores.
 __host__ __device__ constexpr int bm_row(int p) { return 2 * p + 3; }
 __host__ __device__ constexpr int bm_nwords(int p) { return ((2 * p + 5) * bm_row(p) + 2 + 31) / 32; }
@@ -509,7 +509,9 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
     uint8_t* sref = smem;
     uint8_t* scur = smem + a.cur_off;
     uint32_t* bms = reinterpret_cast<uint32_t*>(smem + a.bm_off);
-    constexpr int BST = NWARP * NG + 1;  // interleaved bitmap word stride
+    // interleaved bitmap word stride: groups + 4 keeps the rows 16-byte aligned (one uint4
+    // store initialises 4 groups' words) and a warp's 32/G groups on distinct banks
+    constexpr int BST = NWARP * NG + 4;
     uint32_t* bm = bms + (warp * NG + g);
     uint32_t* bm_init = reinterpret_cast<uint32_t*>(smem + a.init_off);
     int* ctr = reinterpret_cast<int*>(bm_init + a.bm_words);
@@ -577,10 +579,10 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
         const bool have = idx < nbt;
         if (have) take(idx);
         __syncthreads();  // every current row is in registers: the bitmaps may overwrite them
-        // all bitmaps of the CTA at once: word w of every group, dense stores
-        for (int e = threadIdx.x; e < a.bm_words * BST; e += NWARP * 32) {
-            const int w = e / BST;  // constant divisor
-            bms[e] = bm_init[w];
+        // all bitmaps of the CTA at once: word w of every group, dense 16-byte stores
+        for (int e = threadIdx.x; e < a.bm_words * (BST / 4); e += NWARP * 32) {
+            const uint32_t v = bm_init[e / (BST / 4)];  // constant divisor
+            reinterpret_cast<uint4*>(bms)[e] = make_uint4(v, v, v, v);
         }
         __syncthreads();
         if (have) gs.init_search(j, bm, BST, bm_init, a.bm_words, p, false);

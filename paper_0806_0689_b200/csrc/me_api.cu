@@ -147,7 +147,7 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     L.TW = TW; L.TH = TH;
     // the ONE kernels (one block per lane group) exist for the default geometry
     L.one = tbx * tby <= groups && L.G == (B == 16 ? 8 : 2) && L.NW == (B == 16 ? 8 : 4);
-    const int bm_bytes = (groups + 1) * a.bm_words * 4;  // interleaved, word stride groups + 1
+    const int bm_bytes = (groups + 4) * a.bm_words * 4;  // interleaved, word stride groups + 4
     if (L.one) {  // bitmaps overlay the current tile (read into registers first)
         a.bm_off = a.cur_off;
         a.init_off = a.cur_off + ((std::max(TW * TH, bm_bytes) + 15) & ~15);
