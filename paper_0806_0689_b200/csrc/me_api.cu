@@ -165,7 +165,13 @@ void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap
     constexpr int DG = B == 16 ? 8 : 2, DNW = B == 16 ? 8 : 4;  // default geometry
     if constexpr (G == DG) {
         if (L.one) {
-            me::dcds_kernel<B, G, DNW, VARIANT, false, true><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
+            // the bench geometries (B=8: 16x4 tiles, +-16; B=16: 8x4 tiles, +-32) also exist
+            // with the region pitch as a constant (immediate row offsets in the loads)
+            constexpr int PC = B == 16 ? 240 : 208;
+            if (L.a.pitch == PC)
+                me::dcds_kernel<B, G, DNW, VARIANT, false, true, PC><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
+            else
+                me::dcds_kernel<B, G, DNW, VARIANT, false, true><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
             return;
         }
     }
@@ -436,6 +442,10 @@ int me_init(int device) {
     if ((rc = allow_smem(me::dcds_kernel<B, G, 8, V>))) return rc;
     ME_DCDS_KERNELS(ME_ALLOW)
 #undef ME_ALLOW
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, false, true, 208>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, false, true, 208>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true, 240>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true, 240>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, false, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, false, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true>))) return rc;
