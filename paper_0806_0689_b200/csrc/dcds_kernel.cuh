@@ -490,9 +490,10 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
                 const SearchArgs a) {
     static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "lane-group size");
     constexpr int NG = 32 / G;    // groups per warp (rows per lane and words per row: GroupState)
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    __shared__ __align__(8) uint64_t s_bar;
-    uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
+    // all shared memory is dynamic, from a 1024-aligned base (TMA destinations are 128-byte
+    // aligned; the launch fails loudly otherwise)
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if ((smem_u32(smem) & 127) != 0) __trap();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = lane % G, g = lane / G, leader = g * G;
     const int pair = blockIdx.z;
@@ -515,14 +516,15 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
     uint32_t* bm = bms + (warp * NG + g);
     uint32_t* bm_init = reinterpret_cast<uint32_t*>(smem + a.init_off);
     int* ctr = reinterpret_cast<int*>(bm_init + a.bm_words);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((a.init_off + 4 * a.bm_words + 4 + 7) & ~7));
 
     // ---- stage the tile with TMA: reference region + current tile, one mbarrier
-    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    if (threadIdx.x == 0) mbar_init(bar, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
-        mbar_expect_tx(&s_bar, (uint32_t)(pitch * a.rh + TW * TH));
-        tma_load_3d(sref, &tm_ref, xs, ys, pair, &s_bar);
-        tma_load_3d(scur, &tm_cur, x0, y0, pair, &s_bar);
+        mbar_expect_tx(bar, (uint32_t)(pitch * a.rh + TW * TH));
+        tma_load_3d(sref, &tm_ref, xs, ys, pair, bar);
+        tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
         *ctr = 0;
     }
     const int bw = bm_row(p);
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
         for (int rs = (lo / bw) * bw; rs < lo + 32; rs += bw) w |= span(rs, rs + 2);
         bm_init[t] = w;
     }
-    mbar_wait(&s_bar, 0);
+    mbar_wait(bar, 0);
     if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
         fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
     __syncthreads();

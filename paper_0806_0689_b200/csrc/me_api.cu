@@ -155,7 +155,8 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
         a.bm_off = a.cur_off + TW * TH;
         a.init_off = a.bm_off + ((bm_bytes + 15) & ~15);
     }
-    L.smem = 128 + (size_t)a.init_off + (size_t)a.bm_words * 4 + 16;
+    // template words, tile counter, mbarrier (8-byte aligned)
+    L.smem = (size_t)((a.init_off + 4 * a.bm_words + 4 + 7) & ~7) + 8;
     if (const char* e = getenv("ME_SMEM_PAD")) L.smem += (size_t)std::max(0, atoi(e));  // tuning only
     return L;
 }
