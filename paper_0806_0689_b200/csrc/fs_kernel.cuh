@@ -41,7 +41,7 @@ struct FsArgs {
 // consecutive dx, which the copy stride spreads over all 32 banks.  Per-block argmin:
 // shared-memory atomicMin on (SAD << 13 | rank) keys (reading C13).
 template <int B>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
     fs_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
               const FsArgs a) {
     constexpr int W4 = B / 4;
@@ -118,6 +118,21 @@ __global__ void __launch_bounds__(256)
         const int c1 = min(a.nch, (sp + 1) * cps);
         for (int c = sp * cps; c < c1; c++) {
             const uint32_t* rb = base + (c * B) * pw;  // region row of (dy = c*B - p, i = 0)
+            const uint32_t r0 = (uint32_t)(1 + c * B * side + dxp);
+            if ((c + 1) * B > side) {
+                // the last chunk holds side - c*B < B candidates: score them one by one (a
+                // full chunk would spend B*B*W4 VABSDIFF4 on rows past dy = p)
+                const int nd = side - c * B;
+                for (int d = 0; d < nd; d++) {
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int i = 0; i < B; i++)
+#pragma unroll
+                        for (int w = 0; w < W4; w++) acc = vsad4(cw[i][w], rb[(d + i) * pw + w], acc);
+                    key = min(key, (acc << 13) + (r0 + (uint32_t)(d * side)));
+                }
+                continue;
+            }
             uint32_t acc[B];
 #pragma unroll
             for (int d = 0; d < B; d++) acc[d] = 0;
@@ -137,16 +152,8 @@ __global__ void __launch_bounds__(256)
             }
             // raster ranks 1 + (dy+p)(2p+1) + (dx+p) for every candidate, (0,0) included; the
             // centre-first rule (reading C13) is applied once per block in the output phase
-            const uint32_t r0 = (uint32_t)(1 + c * B * side + dxp);
-            if ((c + 1) * B <= side) {
 #pragma unroll
-                for (int d = 0; d < B; d++) key = min(key, (acc[d] << 13) + (r0 + (uint32_t)(d * side)));
-            } else {  // the last chunk: rows past dy = p are padding
-                const int nd = side - c * B;
-#pragma unroll
-                for (int d = 0; d < B; d++)
-                    if (d < nd) key = min(key, (acc[d] << 13) + (r0 + (uint32_t)(d * side)));
-            }
+            for (int d = 0; d < B; d++) key = min(key, (acc[d] << 13) + (r0 + (uint32_t)(d * side)));
         }
         atomicMin(&s_key[b], key);
     }

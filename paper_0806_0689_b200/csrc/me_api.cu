@@ -327,7 +327,7 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
     int tbx = B == 16 ? 4 : 8, tby = 4;
     auto fs_smem = [&](int tx, int ty) {
         const int pt = ((tx * B + 2 * p + 31) + 15) & ~15;
-        const int rp = std::max(ty * B + 2 * p, (ty + a.nch) * B - 1);
+        const int rp = ty * B + 2 * p;
         return 4 * ((pt * rp + 127 + 128 * 4) & ~127) + tx * ty * B * B + 1024;
     };
     while ((tbx > 1 || tby > 1) &&
@@ -348,7 +348,9 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
     const int TW = tbx * B, TH = tby * B;
     a.pitch = ((TW + 2 * p + 31) + 15) & ~15;
     a.rh = TH + 2 * p;
-    a.rh_pad = std::max(a.rh, (tby + a.nch) * B - 1);  // rows the chunked dy loop touches
+    // the chunked dy loop touches rows < rh only (the last, partial chunk is scored candidate
+    // by candidate), so the copies need no padding rows
+    a.rh_pad = a.rh;
     // measured on B200 (profiles/r1b): 8x8 blocks keep a (block, dx) item whole; 16x16 blocks
     // (64 cur registers, 16 accumulators per item) split it into one item per dy chunk
     a.nsplit = B == 16 ? a.nch : 1;
@@ -372,8 +374,13 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
     if (rc) return rc;
     if (stats) CK(cudaMemsetAsync(stats, 0, sizeof(uint64_t) * 3 * (size_t)npairs, s));
     dim3 grid(a.ntx * nty, npairs);
-    if (block == 16) me::fs_kernel<16><<<grid, 256, smem, s>>>(tc, tr, a);
-    else me::fs_kernel<8><<<grid, 256, smem, s>>>(tc, tr, a);
+    int nthr = 256;
+    if (const char* e = getenv("ME_FS_THREADS")) {  // tuning only
+        const int t = atoi(e);
+        if (t >= 64 && t <= 512 && t % 32 == 0) nthr = t;
+    }
+    if (block == 16) me::fs_kernel<16><<<grid, nthr, smem, s>>>(tc, tr, a);
+    else me::fs_kernel<8><<<grid, nthr, smem, s>>>(tc, tr, a);
     g_launches++;
     CK(cudaGetLastError());
     return ME_OK;
