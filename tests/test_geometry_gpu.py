@@ -1,0 +1,105 @@
+"""GPU parity of the DCDS kernels under every launch geometry the library can take.
+
+The default geometry runs the one-block-per-lane-group kernels (`ONE`, with a compile-time
+region pitch at the bench shapes); the tuning knobs ME_G / ME_NW / ME_TILE select the hand-out
+kernels (blocks taken from a tile counter as groups finish) or ONE kernels with idle groups.
+Every geometry must give the oracle's outputs bit for bit (readings C5-C9).
+The knobs are read by the library at every launch (getenv), so the tests set them in-process.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_0806_0689_b200 as me
+from paper_0806_0689_b200 import synth
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
+KNOBS = ("ME_G", "ME_NW", "ME_TILE")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def init():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    me.me_init(0)
+    me.me_set_stream(torch.cuda.current_stream())
+    yield
+
+
+@pytest.fixture
+def knobs():
+    saved = {k: os.environ.get(k) for k in KNOBS}
+    yield os.environ
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+def run(frames, B, p, variant):
+    n, _, H, W = frames.shape
+    mv, sad, pts, st = me.alloc_outputs(n, (W // B) * (H // B), DEV)
+    (me.me_dcds_s_batch if variant else me.me_dcds_batch)(frames, B, p, mv, sad, pts, st)
+    torch.cuda.synchronize()
+    return (mv.cpu().numpy(), sad.cpu().numpy().astype(np.uint32),
+            pts.cpu().numpy().astype(np.uint16), st.cpu().numpy().astype(np.uint64))
+
+
+def check(frames, B, p, variant, tag):
+    host = frames.cpu().numpy()
+    mv, sad, pts, st = run(frames, B, p, variant)
+    for t in range(host.shape[0]):
+        omv, osad, opts = oracle.dcds(host[t, 0], host[t, 1], B, p, variant)
+        bad = np.flatnonzero((mv[t] != omv).any(1) | (sad[t] != osad) | (pts[t] != opts))
+        assert bad.size == 0, f"{tag} pair {t}: {bad.size} blocks differ, first {bad[:5]}"
+        assert st[t, 0] == opts.astype(np.int64).sum() and st[t, 1] == osad.astype(np.int64).sum()
+        assert int(st[t, 2]) == oracle.mc_psnr(host[t, 0], host[t, 1], B, omv)[1]
+
+
+GEOMS = [
+    # (block, {knob: value}) -- hand-out kernels and ONE kernels with idle groups
+    (8, {"ME_TILE": "16,8"}),            # G=2, 4 warps, 128 blocks for 64 groups: hand-out
+    (8, {"ME_TILE": "8,2"}),             # ONE with 48 idle groups
+    (8, {"ME_G": "1", "ME_TILE": "8,4"}),
+    (8, {"ME_G": "4"}),
+    (8, {"ME_G": "8", "ME_NW": "2"}),
+    (8, {"ME_NW": "8", "ME_TILE": "16,4"}),
+    (16, {"ME_TILE": "8,8"}),            # G=8, 8 warps, 64 blocks for 32 groups: hand-out
+    (16, {"ME_TILE": "4,2"}),            # ONE with idle groups
+    (16, {"ME_G": "4", "ME_NW": "4"}),
+    (16, {"ME_G": "2", "ME_TILE": "4,4"}),
+    (8, {}),                             # the defaults (ONE)
+    (16, {}),
+]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("B,env", GEOMS, ids=[f"B{b}-" + ("_".join(f"{k[3:]}{v}" for k, v in e.items()) or "default") for b, e in GEOMS])
+def test_geometry_parity(knobs, B, env, variant):
+    for k in KNOBS:
+        knobs.pop(k, None)
+    knobs.update(env)
+    cfg = synth.CONFIGS["c1"]
+    fr = synth.make_sequence(cfg, device=DEV, pairs=[1, 7, 13])
+    for p in (1, 7, 16):
+        check(fr, B, p, variant, f"B={B} {env} p={p} v={variant}")
+
+
+@pytest.mark.parametrize("B,p", [(8, 16), (16, 32)])
+def test_bench_shapes_with_handout(knobs, B, p):
+    """The bench shapes (compile-time pitch in the ONE kernels) against the hand-out kernels
+    at the same tile height: identical outputs."""
+    for k in KNOBS:
+        knobs.pop(k, None)
+    cfg = synth.CONFIGS["c3" if B == 8 else "c4"]
+    fr = synth.make_sequence(cfg, device=DEV, pairs=[1, 2])
+    ref = run(fr, B, p, 0)
+    knobs["ME_TILE"] = "16,8" if B == 8 else "8,8"
+    got = run(fr, B, p, 0)
+    for a, b in zip(ref, got):
+        np.testing.assert_array_equal(a, b)
