@@ -111,9 +111,9 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     }
 
     // measured on B200 (profiles/r1/SUMMARY.md): B=8: G=2, 4 warps, 16x4 blocks;
-    // B=16: G=8, 8 warps, 8x4 blocks
-    int tbx = (B == 16) ? 8 : 16;
-    int tby = 4;
+    // B=16: G=8, 8 warps, 4x8 blocks (profiles/r1c/SUMMARY.md)
+    int tbx = (B == 16) ? 4 : 16;
+    int tby = (B == 16) ? 8 : 4;
     if (const char* e = getenv("ME_G")) {
         const int g = atoi(e);
         if (g == 1 || g == 2 || g == 4 || g == 8) L.G = g;
@@ -166,9 +166,9 @@ void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap
     constexpr int DG = B == 16 ? 8 : 2, DNW = B == 16 ? 8 : 4;  // default geometry
     if constexpr (G == DG) {
         if (L.one) {
-            // the bench geometries (B=8: 16x4 tiles, +-16; B=16: 8x4 tiles, +-32) also exist
+            // the bench geometries (B=8: 16x4 tiles, +-16; B=16: 4x8 tiles, +-32) also exist
             // with the region pitch as a constant (immediate row offsets in the loads)
-            constexpr int PC = B == 16 ? 240 : 208;
+            constexpr int PC = B == 16 ? 176 : 208;
             if (L.a.pitch == PC)
                 me::dcds_kernel<B, G, DNW, VARIANT, false, true, PC><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
             else
@@ -452,8 +452,8 @@ int me_init(int device) {
 #undef ME_ALLOW
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, false, true, 208>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, false, true, 208>))) return rc;
-    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true, 240>))) return rc;
-    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true, 240>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true, 176>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true, 176>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, false, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, false, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true>))) return rc;
