@@ -1,8 +1,8 @@
 // bma_kernel.cuh -- the paper's comparison block-matching algorithms on sm_100a (SURVEY 8(f)
 // row 3): CDS (ref. [13]), DS (ref. [10]), h-HEXBS (ref. [12], Fig. 2a) and v-HEXBS (Fig. 2b,
 // P:43), on the same engine as the DCDS kernel (dcds_kernel.cuh): TMA-staged tile, lane groups
-// of G lanes per block with hand-out, per-group visited bitmap (reading C5), window-only
-// feasibility over the edge-replicated reference (C8, C9), strict compare (C6), fused
+// of G lanes with one block each, per-group bordered visited bitmap (reading C5; window-only
+// feasibility, C8) over the edge-replicated reference (C9), strict compare (C6), fused
 // motion-compensated SSE and per-pair statistics.
 //
 // Readings (C23-C26, pinned by Table VII's CDS and DS blocks):
@@ -74,11 +74,12 @@ struct BmaArgs {
     const uint8_t* ref0;
     long long stride;
     int W, H, p;
-    int tbx, tby, ntx;
+    int tbx, tby;
     int pitch, rh;
-    int cur_off;
+    int cur_off;            // current tile (TMA destination); the group bitmaps overlay it
+    int init_off;           // bitmap template, row tables, mbarrier
     int bm_words;
-    int nbx, nb;
+    int nbx, nby, nb;
     uint32_t* mv;
     uint32_t* sad;
     uint16_t* pts;
@@ -132,6 +133,11 @@ __device__ __forceinline__ int bma_next(int alg, int r, int& cx, int& cy, int bx
     }
 }
 
+// One CTA per tile of TBX x TBY blocks, exactly one block per lane group (the geometry of the
+// DCDS kernels' ONE path, dcds_kernel.cuh): every group reads its current rows into registers,
+// the CTA overwrites the current tile with the groups' visited bitmaps (interleaved, bordered:
+// a point outside the window reads as visited, reading C8), the groups run their searches,
+// and one dense phase after the last search of a warp computes the SSEs and outputs.
 template <int B, int G, int NWARP, int ALG>
 __global__ void __launch_bounds__(NWARP * 32)
     bma_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
@@ -140,32 +146,34 @@ __global__ void __launch_bounds__(NWARP * 32)
     constexpr int W4 = B / 4;     // 32-bit words per block row
     constexpr int NG = 32 / G;    // groups per warp
     constexpr int NH = G >= 4 ? 1 : 4 / G;
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    __shared__ int4 s_off[NROW];
-    __shared__ uint32_t s_code[NROW];
-    __shared__ __align__(8) uint64_t s_bar;
-    __shared__ int s_ctr;
-    uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
+    constexpr int BST = NWARP * NG + 4;  // interleaved bitmap word stride
+    extern __shared__ __align__(1024) uint8_t smem[];
+    if ((smem_u32(smem) & 127) != 0) __trap();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = lane % G, g = lane / G, leader = g * G;
-    const int pair = blockIdx.y;
-    const int tx = blockIdx.x % a.ntx, ty = blockIdx.x / a.ntx;
+    const int pair = blockIdx.z;
+    const int tx = blockIdx.x, ty = blockIdx.y;
     const int TW = a.tbx * B, TH = a.tby * B;
     const int x0 = tx * TW, y0 = ty * TH;
     const int xs = (x0 - a.p) & ~15;
     const int ys = y0 - a.p;
-    const int pitch = a.pitch, p = a.p, side = 2 * p + 1;
+    const int pitch = a.pitch, p = a.p;
+    const int bw = bm_row(p), c0 = (p + 2) * bw + p + 2;  // bitmap row length, bit of (0,0)
     uint8_t* sref = smem;
     uint8_t* scur = smem + a.cur_off;
-    uint32_t* bm = reinterpret_cast<uint32_t*>(scur + TW * TH) + (warp * NG + g) * a.bm_words;
+    uint32_t* bms = reinterpret_cast<uint32_t*>(scur);
+    uint32_t* bm = bms + (warp * NG + g);
+    uint32_t* bm_init = reinterpret_cast<uint32_t*>(smem + a.init_off);
+    int4* s_off = reinterpret_cast<int4*>(smem + ((a.init_off + 4 * a.bm_words + 15) & ~15));
+    uint32_t* s_code = reinterpret_cast<uint32_t*>(s_off + NROW);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(s_code + NROW + (NROW & 1));
 
-    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    if (threadIdx.x == 0) mbar_init(bar, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
-        mbar_expect_tx(&s_bar, (uint32_t)(pitch * a.rh + TW * TH));
-        tma_load_3d(sref, &tm_ref, xs, ys, pair, &s_bar);
-        tma_load_3d(scur, &tm_cur, x0, y0, pair, &s_bar);
-        s_ctr = 0;
+        mbar_expect_tx(bar, (uint32_t)(pitch * a.rh + TW * TH));
+        tma_load_3d(sref, &tm_ref, xs, ys, pair, bar);
+        tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
     }
     for (int r = threadIdx.x; r < NROW; r += NWARP * 32) {
         const uint32_t w = a.rcode[r];
@@ -173,60 +181,60 @@ __global__ void __launch_bounds__(NWARP * 32)
         s_off[r] = make_int4(rc_dy(w, 0) * pitch + rc_dx(w, 0), rc_dy(w, 1) * pitch + rc_dx(w, 1),
                              rc_dy(w, 2) * pitch + rc_dx(w, 2), rc_dy(w, 3) * pitch + rc_dx(w, 3));
     }
-    mbar_wait(&s_bar, 0);
+    // bitmap template: border bits set (rows < 2 or >= 2p+3, columns < 2 of the row length)
+    for (int t = threadIdx.x; t < a.bm_words; t += NWARP * 32) {
+        const int lo = 32 * t;
+        auto span = [lo](int b0, int b1) -> uint32_t {
+            b0 = max(b0, lo); b1 = min(b1, lo + 32);
+            return b1 > b0 ? (uint32_t)(((1ull << (b1 - b0)) - 1ull) << (b0 - lo)) : 0u;
+        };
+        uint32_t w = span(0, 2 * bw) | span((2 * p + 3) * bw, lo + 32);
+        for (int rs = (lo / bw) * bw; rs < lo + 32; rs += bw) w |= span(rs, rs + 2);
+        bm_init[t] = w;
+    }
+    mbar_wait(bar, 0);
     if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
         fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
     __syncthreads();
 
     const uint32_t* s = reinterpret_cast<const uint32_t*>(sref);
     const int rstride = G * pitch, jrow = j * pitch;
-    const int nby = a.nb / a.nbx;
-    const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, nby - ty * a.tby);
+    const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, a.nby - ty * a.tby);
     const int nbt = tbx_e * tby_e;
 
     // group state (identical in the G lanes of a group)
-    bool act = false;
-    int row = 0, cx = 0, cy = 0, bx = 0, by = 0, pts = 0, bofs = 0;
+    const int idx = warp * NG + g;
+    bool act = idx < nbt;
+    const bool have = act;
+    int row = bma_first_row(ALG), cx = 0, cy = 0, bx = 0, by = 0, pts = 0, bofs = 0;
     uint32_t best = 0xffffffffu;
     long long gblk = 0;
     uint32_t cw[R][W4];
+    if (have) {
+        const int lby = idx / tbx_e, lbx = idx - lby * tbx_e;
+        const int bxg = x0 + lbx * B, byg = y0 + lby * B;
+        gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
+        bofs = (byg - ys) * pitch + (bxg - xs);
 #pragma unroll
-    for (int r = 0; r < R; r++)
+        for (int r = 0; r < R; r++) {
+            const uint32_t* crow = reinterpret_cast<const uint32_t*>(scur + (lby * B + j + G * r) * TW + lbx * B);
 #pragma unroll
-        for (int w = 0; w < W4; w++) cw[r][w] = 0;
-    unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
-
-    for (;;) {
-        // ---- idle groups take the next block of the tile
-        const unsigned need = __ballot_sync(FULL, !act && j == 0);
-        if (need && *reinterpret_cast<volatile int*>(&s_ctr) < nbt) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(&s_ctr, __popc(need));
-            base = __shfl_sync(FULL, base, 0);
-            const int idx = __shfl_sync(FULL, base + __popc(need & ((1u << lane) - 1u)), leader);
-            if (!act && idx < nbt) {
-                const int lby = idx / tbx_e, lbx = idx - lby * tbx_e;
-                const int bxg = x0 + lbx * B, byg = y0 + lby * B;
-                gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
-                bofs = (byg - ys) * pitch + (bxg - xs);
-#pragma unroll
-                for (int r = 0; r < R; r++) {
-                    const uint32_t* crow = reinterpret_cast<const uint32_t*>(scur + (lby * B + j + G * r) * TW + lbx * B);
-#pragma unroll
-                    for (int w = 0; w < W4; w++) cw[r][w] = crow[w];
-                }
-                for (int w = j * 4; w < a.bm_words; w += 4 * G)
-                    *reinterpret_cast<uint4*>(bm + w) = make_uint4(0, 0, 0, 0);
-                act = true;
-                row = bma_first_row(ALG);
-                cx = cy = bx = by = 0;
-                pts = 0;
-                best = 0xffffffffu;
-            }
-            __syncwarp();
+            for (int w = 0; w < W4; w++) cw[r][w] = crow[w];
         }
-        if (!__any_sync(FULL, act)) break;
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; r++)
+#pragma unroll
+            for (int w = 0; w < W4; w++) cw[r][w] = 0;
+    }
+    __syncthreads();  // every current row is in registers: the bitmaps may overwrite them
+    for (int e = threadIdx.x; e < a.bm_words * (BST / 4); e += NWARP * 32) {
+        const uint32_t v = bm_init[e / (BST / 4)];
+        reinterpret_cast<uint4*>(bms)[e] = make_uint4(v, v, v, v);
+    }
+    __syncthreads();
 
+    while (__any_sync(FULL, act)) {
         // ---- one row: visited test-and-set, SADs, first strict minimum (C5, C6, C26)
         const uint32_t pw = s_code[row];
         const int4 po = s_off[row];
@@ -237,12 +245,10 @@ __global__ void __launch_bounds__(NWARP * 32)
             const int k = j + h * G;
             bool nw = false;
             if (k < 4 && ((used >> k) & 1)) {
-                const int qx = cx + rc_dx(pw, k), qy = cy + rc_dy(pw, k);
-                if (qx >= -p && qx <= p && qy >= -p && qy <= p) {
-                    const int idx = (qy + p) * side + (qx + p);
-                    const uint32_t bit = 1u << (idx & 31);
-                    nw = (atomicOr(&bm[idx >> 5], bit) & bit) == 0;
-                }
+                // the border bits make points outside the window read as visited (C8)
+                const int bi = c0 + (cy + rc_dy(pw, k)) * bw + (cx + rc_dx(pw, k));
+                const uint32_t bit = 1u << (bi & 31);
+                nw = (atomicOr(&bm[(bi >> 5) * BST], bit) & bit) == 0;
             }
             const unsigned bb = __ballot_sync(FULL, nw) >> leader;
             m4 |= (G >= 4 ? (bb & 0xfu) : ((bb & ((1u << G) - 1u)) << (h * G)));
@@ -275,7 +281,6 @@ __global__ void __launch_bounds__(NWARP * 32)
 #pragma unroll
         for (int k = 0; k < 4; k++)
             if ((m4 >> k) & 1) key = min(key, (sadk[k] << 2) | k);
-        bool fin = false;
         if (act) {
             pts += __popc(m4);
             // CDS step 2 prefers the central 3x3 square: a tie with m moves the BMP (C23)
@@ -286,35 +291,31 @@ __global__ void __launch_bounds__(NWARP * 32)
                 by = cy + rc_dy(pw, key & 3);
             }
             const int nr = bma_next(ALG, row, cx, cy, bx, by);
-            if (nr < 0) fin = true;
+            if (nr < 0) act = false;
             else row = nr;
         }
+    }
 
-        // ---- finished blocks: SSE at the MV (P:342 aspect 4), outputs
-        if (__any_sync(FULL, fin)) {
-            uint32_t ss = 0;
-            if (fin) {
-                uint32_t rw[R][W4];
-                ref_rows<R, W4>(s, bofs + by * pitch + bx + jrow, rstride, rw);
+    // ---- every search of the warp ended: SSE at the MV (P:342 aspect 4), outputs, stats
+    uint32_t ss = 0;
+    if (have) {
+        uint32_t rw[R][W4];
+        ref_rows<R, W4>(s, bofs + by * pitch + bx + jrow, rstride, rw);
 #pragma unroll
-                for (int r = 0; r < R; r++)
+        for (int r = 0; r < R; r++)
 #pragma unroll
-                    for (int w = 0; w < W4; w++) ss = ssd4(cw[r][w], rw[r][w], ss);
-            }
+            for (int w = 0; w < W4; w++) ss = ssd4(cw[r][w], rw[r][w], ss);
+    }
 #pragma unroll
-            for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
-            if (fin) {
-                if (j == 0) {
-                    a.mv[gblk] = (uint32_t)(bx & 0xffff) | ((uint32_t)by << 16);
-                    a.sad[gblk] = best;
-                    a.pts[gblk] = (uint16_t)pts;
-                    acc_pts += (unsigned)pts;
-                    acc_sad += best;
-                    acc_sse += ss;
-                }
-                act = false;
-            }
-        }
+    for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
+    unsigned long long acc_pts = 0, acc_sad = 0, acc_sse = 0;
+    if (have && j == 0) {
+        a.mv[gblk] = (uint32_t)(bx & 0xffff) | ((uint32_t)by << 16);
+        a.sad[gblk] = best;
+        a.pts[gblk] = (uint16_t)pts;
+        acc_pts = (unsigned)pts;
+        acc_sad = best;
+        acc_sse = ss;
     }
     if (a.stats) {
 #pragma unroll

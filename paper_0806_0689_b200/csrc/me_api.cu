@@ -274,31 +274,33 @@ void launch_bma_b(int alg, dim3 grid, size_t smem, const CUtensorMap& tc, const 
 int run_bma(int alg, const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W,
             int H, int block, int p, int16_t* mv, uint32_t* sad, uint16_t* pts, uint64_t* stats,
             cudaStream_t s) {
-    // geometry of the DCDS defaults (B=8: G=2, 4 warps, 16x4 tiles; B=16: G=8, 8 warps, 8x4)
+    // the DCDS default geometry (B=8: G=2, 4 warps, 16x4 tiles; B=16: G=8, 8 warps, 4x8):
+    // one block per lane group
     const int B = block, nbx = W / B, nby = H / B;
     const int G = B == 16 ? 8 : 2, NW = B == 16 ? 8 : 4;
-    int tbx = std::min(B == 16 ? 8 : 16, nbx), tby = std::min(4, nby);
+    int tbx = std::min(B == 16 ? 4 : 16, nbx), tby = std::min(B == 16 ? 8 : 4, nby);
     while ((tbx * B) % 16) tbx++;
     me::BmaArgs a;
     a.cur0 = cur0; a.ref0 = ref0; a.stride = stride;
     a.W = W; a.H = H; a.p = p;
     a.tbx = tbx; a.tby = tby;
-    a.ntx = (nbx + tbx - 1) / tbx;
-    const int nty = (nby + tby - 1) / tby;
+    const int ntx = (nbx + tbx - 1) / tbx, nty = (nby + tby - 1) / tby;
     const int TW = tbx * B, TH = tby * B;
     int pitch = ((TW + 2 * p + 31) + 15) & ~15;
     if (((pitch >> 4) & 1) == 0) pitch += 16;
     a.pitch = pitch;
     a.rh = TH + 2 * p;
-    const int side = 2 * p + 1;
-    a.bm_words = (((side * side + 31) / 32) + 3) & ~3;
-    a.nbx = nbx; a.nb = nbx * nby;
-    a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;
+    a.bm_words = me::bm_nwords(p);
+    a.nbx = nbx; a.nby = nby; a.nb = nbx * nby;
     a.mv = reinterpret_cast<uint32_t*>(mv); a.sad = sad; a.pts = pts;
     a.stats = reinterpret_cast<unsigned long long*>(stats);
     for (int r = 0; r < me::NROW; r++) a.rcode[r] = me::row_code(r);
     const int groups = NW * 32 / G;
-    const size_t smem = 128 + (size_t)a.cur_off + (size_t)TW * TH + (size_t)groups * a.bm_words * 4 + 32;
+    a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;
+    a.init_off = a.cur_off + ((std::max(TW * TH, (groups + 4) * a.bm_words * 4) + 15) & ~15);
+    // template words | row offsets (int4, 16-aligned) | row codes | mbarrier (8-aligned)
+    const size_t tables = (size_t)((a.init_off + 4 * a.bm_words + 15) & ~15) + 16 * me::NROW + 4 * (me::NROW + (me::NROW & 1));
+    const size_t smem = tables + 8;
     if ((int)smem > g_smem_optin) return fail(ME_EINVAL, "tile does not fit in shared memory");
     CUtensorMap tc, tr;
     int rc = make_tmap(&tc, cur0, W, H, npairs, stride, TW, TH);
@@ -306,7 +308,7 @@ int run_bma(int alg, const uint8_t* cur0, const uint8_t* ref0, long long stride,
     rc = make_tmap(&tr, ref0, W, H, npairs, stride, a.pitch, a.rh);
     if (rc) return rc;
     if (stats) CK(cudaMemsetAsync(stats, 0, sizeof(uint64_t) * 3 * (size_t)npairs, s));
-    const dim3 grid(a.ntx * nty, npairs);
+    const dim3 grid(ntx, nty, npairs);
     if (B == 16) launch_bma_b<16, 8, 8>(alg, grid, smem, tc, tr, a, s);
     else launch_bma_b<8, 2, 4>(alg, grid, smem, tc, tr, a, s);
     g_launches++;
