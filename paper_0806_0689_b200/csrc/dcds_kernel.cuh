@@ -258,7 +258,9 @@ struct GroupState {
     // centre (dx, dy) from its bitmap bit (the row length exceeds 2p + 1)
     __device__ __forceinline__ void centre(int p, int& cx, int& cy) const {
         const int bw = bm_row(p);
-        const int row = cidx / bw;
+        // cidx / bw by a float quotient: cidx < 2^13 and the quotient stays >= 0.5/bw from an
+        // integer, far above the error of the approximate division
+        const int row = (int)__fdividef((float)cidx + 0.5f, (float)bw);
         cy = row - p - 2;
         cx = cidx - row * bw - p - 2;
     }
@@ -304,8 +306,8 @@ struct GroupState {
     // in Step 3 (switching strategy one) or, on the halfway stop, in a Step-4
     // state with no slots, which the next pass finishes.  All lanes of the warp call it (and
     // __syncwarp after it).
-    __device__ __forceinline__ void step1(const uint32_t* s, uint32_t* bm, int bst, int j, int p,
-                                          int pitch, int rstride, int jrow) {
+    __device__ __forceinline__ void step1(const uint32_t* s, int j, int p, int pitch, int rstride,
+                                          int jrow) {
         const bool live = (st == ST_S1A);
         uint32_t sk[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
         if (live) {
@@ -339,15 +341,9 @@ struct GroupState {
             const uint32_t sad = (v[k >> 1] >> (16 * (k & 1))) & 0xffffu;
             if ((feas >> k) & 1) key = min(key, (sad << 3) | k);
         }
-        // visited set (reading C5): the group's first lane marks the scored points
+        // visited set (reading C5): the HCSP points are already set in every group's initial
+        // bitmap (the pattern sits at the window origin for every block)
         const int bw = bm_row(p);
-        if (j == 0) {
-            const int c = cidx;
-            const int idx[7] = {c, c - 1, c + 1, c - 2, c + 2, c - bw, c + bw};
-#pragma unroll
-            for (int k = 0; k < 7; k++)
-                if ((feas >> k) & 1) bm[(idx[k] >> 5) * bst] |= 1u << (idx[k] & 31);
-        }
         pts = __popc(feas);
         best = key >> 3;
         trace(j, 15, feas, 0, 0);
@@ -377,9 +373,9 @@ struct GroupState {
     }
 
     // One pass of the group's state machine; returns true when the block's search ended.
-    // bm_init: the border template (the DCDS^S look-up's window test).
+    // bm_win: the border-only template (the DCDS^S look-up's window test).
     template <int VARIANT>
-    __device__ __forceinline__ bool pass(const uint32_t* s, uint32_t* bm, int bst, const uint32_t* bm_init,
+    __device__ __forceinline__ bool pass(const uint32_t* s, uint32_t* bm, int bst, const uint32_t* bm_win,
                                          int j, int leader, int p, int pitch, int jrow, int rstride) {
         // ---- visited-set test-and-set (reading C5): lane j of a group owns slots j, j+G, ...
         unsigned m4 = 0;
@@ -392,7 +388,7 @@ struct GroupState {
                 const int idx = cidx + ((k & 1) ? de : -de);
                 const uint32_t bit = 1u << (idx & 31);
                 if (VARIANT && st == ST_S4PRE)
-                    nw = (bm_init[idx >> 5] & bit) == 0;  // DCDS^S look-up: in the window
+                    nw = (bm_win[idx >> 5] & bit) == 0;  // DCDS^S look-up: in the window
                 else
                     nw = (atomicOr(&bm[(idx >> 5) * bst], bit) & bit) == 0;
             }
@@ -514,9 +510,10 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
     // store initialises 4 groups' words) and a warp's 32/G groups on distinct banks
     constexpr int BST = NWARP * NG + 4;
     uint32_t* bm = bms + (warp * NG + g);
-    uint32_t* bm_init = reinterpret_cast<uint32_t*>(smem + a.init_off);
-    int* ctr = reinterpret_cast<int*>(bm_init + a.bm_words);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((a.init_off + 4 * a.bm_words + 4 + 7) & ~7));
+    uint32_t* bm_init = reinterpret_cast<uint32_t*>(smem + a.init_off);  // border + HCSP
+    uint32_t* bm_win = bm_init + a.bm_words;                               // border only
+    int* ctr = reinterpret_cast<int*>(bm_win + a.bm_words);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((a.init_off + 8 * a.bm_words + 4 + 7) & ~7));
 
     // ---- stage the tile with TMA: reference region + current tile, one mbarrier
     if (threadIdx.x == 0) mbar_init(bar, 1);
@@ -538,6 +535,13 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
         };
         uint32_t w = span(0, 2 * bw) | span((2 * p + 3) * bw, lo + 32);
         for (int rs = (lo / bw) * bw; rs < lo + 32; rs += bw) w |= span(rs, rs + 2);
+        bm_win[t] = w;
+        // the HCSP points of Step 1, scored by every block at the window origin
+        const int c = (p + 2) * bw + p + 2;
+        const int hc[7] = {c, c - 1, c + 1, c - 2, c + 2, c - bw, c + bw};
+#pragma unroll
+        for (int k = 0; k < 7; k++)
+            if (hc[k] >= lo && hc[k] < lo + 32) w |= 1u << (hc[k] - lo);
         bm_init[t] = w;
     }
     mbar_wait(bar, 0);
@@ -557,7 +561,7 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
 
     // block idx of the tile (row-major over tbx_e columns): its output index and current rows
     auto take = [&](int idx) {
-        const int lby = idx / tbx_e;
+        const int lby = (int)__fdividef((float)idx + 0.5f, (float)tbx_e);  // idx < 2^12: exact
         const int lbx = idx - lby * tbx_e;
         const int bxg = x0 + lbx * B, byg = y0 + lby * B;
         gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
@@ -590,10 +594,10 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
         if (have) gs.init_search(j, bm, BST, bm_init, a.bm_words, p, false);
         else { gs.st = ST_IDLE; gs.want = 0; }
         if (__any_sync(FULL, have)) {
-            gs.step1(s, bm, BST, j, p, pitch, rstride, jrow);
+            gs.step1(s, j, p, pitch, rstride, jrow);
             __syncwarp();  // the visited bits are set before the pass tests them
             while (__any_sync(FULL, gs.st != ST_DONE && gs.st != ST_IDLE))
-                if (gs.template pass<VARIANT>(s, bm, BST, bm_init, j, leader, p, pitch, jrow, rstride)) {
+                if (gs.template pass<VARIANT>(s, bm, BST, bm_win, j, leader, p, pitch, jrow, rstride)) {
                     gs.st = ST_DONE; gs.want = 0;
                 }
             // every search of the warp ended: SSE of the compensated blocks (P:342 aspect 4)
@@ -631,11 +635,11 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
         if (__all_sync(FULL, gs.st == ST_IDLE)) break;
         // ---- groups that just took a block run Step 1 in one straight-line step
         if (__any_sync(FULL, gs.st == ST_S1A)) {
-            gs.step1(s, bm, BST, j, p, pitch, rstride, jrow);
+            gs.step1(s, j, p, pitch, rstride, jrow);
             __syncwarp();  // the visited bits are set before the pass tests them
         }
 
-        const bool fin = gs.template pass<VARIANT>(s, bm, BST, bm_init, j, leader, p, pitch, jrow, rstride);
+        const bool fin = gs.template pass<VARIANT>(s, bm, BST, bm_win, j, leader, p, pitch, jrow, rstride);
 
         // ---- finished blocks: SSE of the compensated block (P:342 aspect 4), outputs
         if (__any_sync(FULL, fin)) {
@@ -649,16 +653,28 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
         }
     }
     if (a.stats) {  // per-pair statistics: warp sums of the group leaders, 3 atomics per warp
+        if constexpr (ONE) {
+            // one block per group: a warp's sums fit 32 bits (<= 32 blocks x 255^2 x 256)
+            const uint32_t sp = __reduce_add_sync(FULL, (uint32_t)acc_pts);
+            const uint32_t sd = __reduce_add_sync(FULL, (uint32_t)acc_sad);
+            const uint32_t se = __reduce_add_sync(FULL, (uint32_t)acc_sse);
+            if (lane == 0) {
+                atomicAdd(&a.stats[pair * 3 + 0], (unsigned long long)sp);
+                atomicAdd(&a.stats[pair * 3 + 1], (unsigned long long)sd);
+                atomicAdd(&a.stats[pair * 3 + 2], (unsigned long long)se);
+            }
+        } else {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            acc_pts += __shfl_xor_sync(FULL, acc_pts, o);
-            acc_sad += __shfl_xor_sync(FULL, acc_sad, o);
-            acc_sse += __shfl_xor_sync(FULL, acc_sse, o);
-        }
-        if (lane == 0) {
-            atomicAdd(&a.stats[pair * 3 + 0], acc_pts);
-            atomicAdd(&a.stats[pair * 3 + 1], acc_sad);
-            atomicAdd(&a.stats[pair * 3 + 2], acc_sse);
+            for (int o = 16; o > 0; o >>= 1) {
+                acc_pts += __shfl_xor_sync(FULL, acc_pts, o);
+                acc_sad += __shfl_xor_sync(FULL, acc_sad, o);
+                acc_sse += __shfl_xor_sync(FULL, acc_sse, o);
+            }
+            if (lane == 0) {
+                atomicAdd(&a.stats[pair * 3 + 0], acc_pts);
+                atomicAdd(&a.stats[pair * 3 + 1], acc_sad);
+                atomicAdd(&a.stats[pair * 3 + 2], acc_sse);
+            }
         }
     }
 }

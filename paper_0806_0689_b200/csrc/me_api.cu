@@ -143,7 +143,9 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     a.nb = nbx * nby;
     L.grid = dim3(a.ntx, nty, npairs);
     const int groups = L.NW * 32 / L.G;
-    a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;  // TMA destinations are 128-byte aligned
+    // TMA destinations are 128-byte aligned; the 3-word row loads never pass the region's
+    // last row (pitch >= TW + 2p + 16 + 15), so nothing needs slack after it
+    a.cur_off = (pitch * a.rh + 127) & ~127;
     L.TW = TW; L.TH = TH;
     // the ONE kernels (one block per lane group) exist for the default geometry
     L.one = tbx * tby <= groups && L.G == (B == 16 ? 8 : 2) && L.NW == (B == 16 ? 8 : 4);
@@ -155,8 +157,8 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
         a.bm_off = a.cur_off + TW * TH;
         a.init_off = a.bm_off + ((bm_bytes + 15) & ~15);
     }
-    // template words, tile counter, mbarrier (8-byte aligned)
-    L.smem = (size_t)((a.init_off + 4 * a.bm_words + 4 + 7) & ~7) + 8;
+    // template words (initial bitmap, window border), tile counter, mbarrier (8-byte aligned)
+    L.smem = (size_t)((a.init_off + 8 * a.bm_words + 4 + 7) & ~7) + 8;  // 2 templates
     if (const char* e = getenv("ME_SMEM_PAD")) L.smem += (size_t)std::max(0, atoi(e));  // tuning only
     return L;
 }
@@ -296,7 +298,7 @@ int run_bma(int alg, const uint8_t* cur0, const uint8_t* ref0, long long stride,
     a.stats = reinterpret_cast<unsigned long long*>(stats);
     for (int r = 0; r < me::NROW; r++) a.rcode[r] = me::row_code(r);
     const int groups = NW * 32 / G;
-    a.cur_off = ((pitch * a.rh + 16) + 127) & ~127;
+    a.cur_off = (pitch * a.rh + 127) & ~127;  // no slack needed (see plan_dcds)
     a.init_off = a.cur_off + ((std::max(TW * TH, (groups + 4) * a.bm_words * 4) + 15) & ~15);
     // template words | row offsets (int4, 16-aligned) | row codes | mbarrier (8-aligned)
     const size_t tables = (size_t)((a.init_off + 4 * a.bm_words + 15) & ~15) + 16 * me::NROW + 4 * (me::NROW + (me::NROW & 1));
