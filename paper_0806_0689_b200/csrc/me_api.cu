@@ -134,7 +134,14 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     const int nty = (nby + tby - 1) / tby;
     // region width: x0 - xs <= p + 15, plus TW + p, plus 16 bytes of over-read slack
     int pitch = ((TW + 2 * p + 31) + 15) & ~15;
-    if (((pitch >> 4) & 1) == 0) pitch += 16;  // 16 * odd bytes: rows spread over the banks
+    // 8x8 blocks: 64 (mod 128) bytes, so the two lanes of a group (rows one pitch apart) read
+    // banks 16 apart -- measured by replaying real search traces through the warp's loads
+    // (tools/sim_banks.py: 1.54 wavefronts per candidate-row load vs 1.77 at 208 bytes);
+    // otherwise (or past the 256-byte TMA box) 16 * odd bytes
+    int p64 = pitch;
+    while ((p64 & 127) != 64) p64 += 16;
+    if (B == 8 && p64 <= 256) pitch = p64;
+    else if (((pitch >> 4) & 1) == 0) pitch += 16;
     a.pitch = pitch;
     a.rh = TH + 2 * p;
     a.bm_words = me::bm_nwords(p);
@@ -170,7 +177,7 @@ void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap
         if (L.one) {
             // the bench geometries (B=8: 16x4 tiles, +-16; B=16: 4x8 tiles, +-32) also exist
             // with the region pitch as a constant (immediate row offsets in the loads)
-            constexpr int PC = B == 16 ? 176 : 208;
+            constexpr int PC = B == 16 ? 176 : 192;
             if (L.a.pitch == PC)
                 me::dcds_kernel<B, G, DNW, VARIANT, false, true, PC><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
             else
@@ -454,8 +461,8 @@ int me_init(int device) {
     if ((rc = allow_smem(me::dcds_kernel<B, G, 8, V>))) return rc;
     ME_DCDS_KERNELS(ME_ALLOW)
 #undef ME_ALLOW
-    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, false, true, 208>))) return rc;
-    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, false, true, 208>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, false, true, 192>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, false, true, 192>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true, 176>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true, 176>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, false, true>))) return rc;
