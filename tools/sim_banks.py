@@ -22,12 +22,17 @@ def decode(rec):
     return pid, mask, cx - 256 if cx > 127 else cx, cy - 256 if cy > 127 else cy
 
 
-def lane_words(layout, pitch, bofs, cpos_off, slot_off):
+def lane_words(layout, pitch, bofs, cpos_off, slot_off, B=8, G=2):
     """word addresses [lanes, loads] of one slot of one group under a layout"""
     o = bofs + cpos_off + slot_off
-    if layout == "row":        # lane j: rows j, j+2, j+4, j+6; 3 words per row
-        base = [(o + j * pitch) >> 2 for j in (0, 1)]
-        return [[b + r * (2 * pitch >> 2) + w for r in range(4) for w in range(3)] for b in base]
+    if layout == "row":        # lane j: rows j, j+G, ...; B/4 + 1 words per row
+        base = [(o + j * pitch) >> 2 for j in range(G)]
+        return [[b + r * (G * pitch >> 2) + w for r in range(B // G) for w in range(B // 4 + 1)] for b in base]
+    if layout == "rowpred":    # as row, the last word only when the row is unaligned
+        base = [(o + j * pitch) >> 2 for j in range(G)]
+        last = B // 4 if (o & 3) else -1
+        return [[b + r * (G * pitch >> 2) + w if w != B // 4 or last >= 0 else -1
+                 for r in range(B // G) for w in range(B // 4 + 1)] for b in base]
     if layout == "half":       # lane j: rows 4j .. 4j+3
         base = [(o + 4 * j * pitch) >> 2 for j in (0, 1)]
         return [[b + r * (pitch >> 2) + w for r in range(4) for w in range(3)] for b in base]
@@ -37,7 +42,7 @@ def lane_words(layout, pitch, bofs, cpos_off, slot_off):
     raise ValueError(layout)
 
 
-def simulate(d, layout="row", pitch=208, warp_shape=(16, 1)):
+def simulate(d, layout="row", pitch=208, warp_shape=(16, 1), G=2, tby=4):
     tr, tl = d["trace"], d["tlen"]
     W, H, B, p = int(d["W"]), int(d["H"]), int(d["B"]), int(d["p"])
     nbx, nby = W // B, H // B
@@ -56,8 +61,8 @@ def simulate(d, layout="row", pitch=208, warp_shape=(16, 1)):
                 bofs = []
                 for a in range(wy):
                     for b in range(wx):
-                        lby = (wy0 + a) % 4
-                        bofs.append((lby * B + p) * pitch + 16 + b * B)
+                        lby = (wy0 + a) % tby
+                        bofs.append((lby * B + p) * pitch + ((p + 15) & ~15) + b * B)
                 for i in range(1, npass):
                     for k in range(4):
                         lanes = []
@@ -66,15 +71,18 @@ def simulate(d, layout="row", pitch=208, warp_shape=(16, 1)):
                                 pid, mask, cx, cy = r[i]
                                 if (mask >> k) & 1:
                                     dx, dy = SLOTS[pid][k]
-                                    lanes += lane_words(layout, pitch, bofs[g], cy * pitch + cx, dy * pitch + dx)
+                                    lanes += lane_words(layout, pitch, bofs[g], cy * pitch + cx, dy * pitch + dx, B, G)
                         if not lanes:
                             continue
                         L = np.array(lanes)  # [lanes, loads]
                         for q in range(L.shape[1]):
-                            words = np.unique(L[:, q])
-                            total_wf += np.bincount(words % 32, minlength=32).max()
+                            col = L[:, q]
+                            col = col[col >= 0]       # predicated-off lanes issue no access
                             total_lds += 1
                             active_lanes += L.shape[0]
+                            if col.size:
+                                words = np.unique(col)
+                                total_wf += np.bincount(words % 32, minlength=32).max()
     nblk = tr.shape[0] * nbx * nby
     return total_wf / nblk, total_lds / nblk, active_lanes / max(total_lds, 1)
 
