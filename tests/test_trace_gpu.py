@@ -105,3 +105,24 @@ def test_trace_rejects_bad_cap():
         tr = torch.zeros(1, cfg.nb, cap, dtype=torch.int64, device=DEV)
         with pytest.raises(me.MEError):
             me.me_dcds_trace_batch(0, fr, cfg.B, cfg.p, mv, sad, pts, tr, tl)
+
+
+@pytest.mark.parametrize("B,tile", [(8, "16,8"), (16, "8,8")])
+def test_trace_handout_kernels_match_oracle(B, tile):
+    """The trace build of the hand-out kernels (tiles with more blocks than lane groups)."""
+    import os
+    old = os.environ.get("ME_TILE")
+    os.environ["ME_TILE"] = tile
+    try:
+        cfg = synth.CONFIGS["c1"]
+        fr = synth.make_sequence(cfg, device=DEV, pairs=[3])
+        host = fr.cpu().numpy()
+        nb = (fr.shape[3] // B) * (fr.shape[2] // B)
+        for variant in (0, 1):
+            out = run_trace(fr, B, 7, variant)
+            check_blocks(host[0], B, 7, variant, tuple(o[0] for o in out), range(0, nb, 5))
+    finally:
+        if old is None:
+            os.environ.pop("ME_TILE", None)
+        else:
+            os.environ["ME_TILE"] = old
