@@ -9,6 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libme.so")
+SO_DEBUG = os.path.join(HERE, "libme_debug.so")  # -DME_DEBUG: device bounds checks
 CSRC = os.path.join(HERE, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -25,26 +26,28 @@ def sources():
                   + [os.path.join(ROOT, "include", "me.h")])
 
 
-def stale() -> bool:
-    if not os.path.exists(SO):
+def stale(so: str = SO) -> bool:
+    if not os.path.exists(so):
         return True
-    t = os.path.getmtime(SO)
+    t = os.path.getmtime(so)
     return any(os.path.getmtime(f) > t for f in sources())
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not stale():
-        return SO
-    tmp = SO + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, *extra, "-o", tmp, os.path.join(CSRC, "me_api.cu")]
+def build(force: bool = False, verbose: bool = False, extra=(), debug: bool = False) -> str:
+    """libme.so, or with debug=True libme_debug.so (ME_DEBUG bounds checks in the kernels)."""
+    so = SO_DEBUG if debug else SO
+    if not force and not stale(so):
+        return so
+    tmp = so + f".tmp{os.getpid()}"
+    cmd = [NVCC, *NVCC_FLAGS, *(["-DME_DEBUG"] if debug else []), *extra, "-o", tmp,
+           os.path.join(CSRC, "me_api.cu")]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True,
-          extra=["-Xptxas", "-v"] if "--ptxas-v" in sys.argv else [])
-    print(SO)
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv,
+                extra=["-Xptxas", "-v"] if "--ptxas-v" in sys.argv else []))

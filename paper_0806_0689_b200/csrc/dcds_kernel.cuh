@@ -32,6 +32,24 @@ namespace me {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// ME_DEBUG builds (libme_debug.so, paper_0806_0689_b200/build.py): bounds checks of every
+// staged-region load and visited-bitmap access, trapping with a message (compute-sanitizer is
+// not available on the GPU pool).  Release builds compile them out.
+#ifdef ME_DEBUG
+#define ME_CHECK(cond)                                                                      \
+    do {                                                                                    \
+        if (!(cond)) {                                                                      \
+            printf("ME_DEBUG check failed %s:%d: %s (block %d,%d,%d thread %d)\n", __FILE__, \
+                   __LINE__, #cond, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);      \
+            __trap();                                                                       \
+        }                                                                                   \
+    } while (0)
+#else
+#define ME_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 struct SearchArgs {
     const uint8_t* cur0;
     const uint8_t* ref0;
@@ -245,6 +263,7 @@ struct GroupState {
     // the pattern's slots are -d0, +d0, -d1, +d1 (reading C7 order): d0 / d1 as byte offsets in
     // the staged region (db0, db1) and as bitmap offsets (de0, de1), set on state changes
     int db0 = 0, db1 = 0, de0 = 0, de1 = 0;
+    int dbg_region = 0, dbg_bits = 0;  // ME_DEBUG: staged-region bytes, bitmap bits
     uint32_t best = 0;
     uint32_t cw[R][W4];
 
@@ -314,6 +333,7 @@ struct GroupState {
 #pragma unroll
             for (int r = 0; r < R; r++) {
                 const int a = bofs + jrow + r * rstride;
+                ME_CHECK(a - pitch - 4 >= 0 && a + pitch + 4 * W4 + 4 <= dbg_region);
                 uint32_t w[W4 + 2], u[W4 + 2], d[W4 + 2];
                 aligned_row<W4>(s, a, w);
                 aligned_row<W4>(s, a - pitch, u);
@@ -363,6 +383,7 @@ struct GroupState {
     // SSE (P:342 aspect 4) of this lane's rows at the current centre.
     __device__ __forceinline__ uint32_t sse_rows(const uint32_t* s, int jrow, int rstride) const {
         uint32_t rw[R][W4];
+        ME_CHECK(cpos + jrow >= 0 && cpos + jrow + (R - 1) * rstride + 4 * W4 + 4 <= dbg_region);
         ref_rows<R, W4>(s, cpos + jrow, rstride, rw);
         uint32_t ss = 0;
 #pragma unroll
@@ -387,6 +408,7 @@ struct GroupState {
                 const int de = (k & 2) ? de1 : de0;
                 const int idx = cidx + ((k & 1) ? de : -de);
                 const uint32_t bit = 1u << (idx & 31);
+                ME_CHECK(idx >= 0 && idx < dbg_bits);
                 if (VARIANT && st == ST_S4PRE)
                     nw = (bm_win[idx >> 5] & bit) == 0;  // DCDS^S look-up: in the window
                 else
@@ -405,6 +427,8 @@ struct GroupState {
             if ((m4 >> k) & 1) {  // slots not scored this pass issue no shared-memory loads
                 const int db = (k & 2) ? db1 : db0;
                 uint32_t rw[R][W4];
+                ME_CHECK(((k & 1) ? o + db : o - db) >= 0 &&
+                         ((k & 1) ? o + db : o - db) + (R - 1) * rstride + 4 * W4 + 4 <= dbg_region);
                 ref_rows<R, W4>(s, (k & 1) ? o + db : o - db, rstride, rw);
                 acc = 0;
 #pragma unroll
@@ -567,6 +591,10 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
         gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
         if (TRACE) { gs.tr = a.trace + gblk * a.tcap; gs.tcap = a.tcap; gs.npass = 0; }
         gs.load_cur((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW, j);
+#ifdef ME_DEBUG
+        gs.dbg_region = pitch * a.rh;
+        gs.dbg_bits = 32 * a.bm_words;
+#endif
     };
     auto output = [&](uint32_t ss) {
         int cx, cy;

@@ -12,7 +12,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libme.so")
+# ME_LIBRARY selects another in-tree build (tests: libme_debug.so, the ME_DEBUG bounds checks)
+SO_PATH = os.environ.get("ME_LIBRARY") or os.path.join(_HERE, "libme.so")
 
 ME_OK, ME_EINVAL, ME_EALIGN, ME_ENOTINIT, ME_ECUDA, ME_ENOMEM = 0, -1, -2, -3, -4, -5
 
