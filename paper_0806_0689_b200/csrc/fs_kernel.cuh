@@ -119,9 +119,10 @@ __global__ void __launch_bounds__(512)
         for (int c = sp * cps; c < c1; c++) {
             const uint32_t* rb = base + (c * B) * pw;  // region row of (dy = c*B - p, i = 0)
             const uint32_t r0 = (uint32_t)(1 + c * B * side + dxp);
-            if ((c + 1) * B > side) {
-                // the last chunk holds side - c*B < B candidates: score them one by one (a
-                // full chunk would spend B*B*W4 VABSDIFF4 on rows past dy = p)
+            if ((c + 1) * B > side && 2 * (side - c * B) <= B) {
+                // the last chunk holds side - c*B <= B/2 candidates: score them one by one (a
+                // full chunk would spend B*B*W4 VABSDIFF4 on rows past dy = p); a fuller last
+                // chunk runs as a full one over padded rows, its extra candidates masked below
                 const int nd = side - c * B;
                 for (int d = 0; d < nd; d++) {
                     uint32_t acc = 0;
@@ -152,8 +153,15 @@ __global__ void __launch_bounds__(512)
             }
             // raster ranks 1 + (dy+p)(2p+1) + (dx+p) for every candidate, (0,0) included; the
             // centre-first rule (reading C13) is applied once per block in the output phase
+            if ((c + 1) * B <= side) {
 #pragma unroll
-            for (int d = 0; d < B; d++) key = min(key, (acc[d] << 13) + (r0 + (uint32_t)(d * side)));
+                for (int d = 0; d < B; d++) key = min(key, (acc[d] << 13) + (r0 + (uint32_t)(d * side)));
+            } else {  // a fuller last chunk: rows past dy = p are padding
+                const int nd = side - c * B;
+#pragma unroll
+                for (int d = 0; d < B; d++)
+                    if (d < nd) key = min(key, (acc[d] << 13) + (r0 + (uint32_t)(d * side)));
+            }
         }
         atomicMin(&s_key[b], key);
     }

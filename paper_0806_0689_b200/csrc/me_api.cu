@@ -338,7 +338,8 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
     int tbx = B == 16 ? 4 : 8, tby = 4;
     auto fs_smem = [&](int tx, int ty) {
         const int pt = ((tx * B + 2 * p + 31) + 15) & ~15;
-        const int rp = ty * B + 2 * p;
+        const int nd = side - (a.nch - 1) * B;
+        const int rp = 2 * nd <= B ? ty * B + 2 * p : std::max(ty * B + 2 * p, (ty + a.nch) * B - 1);
         return 4 * ((pt * rp + 127 + 128 * 4) & ~127) + tx * ty * B * B + 1024;
     };
     while ((tbx > 1 || tby > 1) &&
@@ -359,9 +360,10 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
     const int TW = tbx * B, TH = tby * B;
     a.pitch = ((TW + 2 * p + 31) + 15) & ~15;
     a.rh = TH + 2 * p;
-    // the chunked dy loop touches rows < rh only (the last, partial chunk is scored candidate
-    // by candidate), so the copies need no padding rows
-    a.rh_pad = a.rh;
+    // a last dy chunk of <= B/2 candidates is scored candidate by candidate and touches rows
+    // < rh only; a fuller one runs as a full chunk over padding rows
+    const int nd_last = side - (a.nch - 1) * B;
+    a.rh_pad = 2 * nd_last <= B ? a.rh : std::max(a.rh, (tby + a.nch) * B - 1);
     // measured on B200 (profiles/r1b): 8x8 blocks keep a (block, dx) item whole; 16x16 blocks
     // (64 cur registers, 16 accumulators per item) split it into one item per dy chunk
     a.nsplit = B == 16 ? a.nch : 1;
