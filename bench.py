@@ -321,7 +321,9 @@ def main():
     flats = [mdist.alloc_flat(n, cfg.nb, dev) for _ in range(nbuf)]
     views = [mdist.flat_views(f, n, cfg.nb) for f in flats]
     outs = [mdist.alloc_flat(n, cfg.nb, dev, ws) for _ in range(nbuf)] if ws > 1 else None
-    comm = torch.cuda.Stream(dev) if ws > 1 else None
+    # high priority: the gather's NCCL blocks get SM slots as soon as search CTAs retire,
+    # instead of waiting for the (many-wave) search grid to drain
+    comm = torch.cuda.Stream(dev, priority=-1) if ws > 1 else None
     ready = [torch.cuda.Event() for _ in range(nbuf)]
     freed = [torch.cuda.Event() for _ in range(nbuf)]
     used = [False] * nbuf
