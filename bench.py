@@ -318,9 +318,12 @@ def main():
     # outputs: one flat buffer [mv | sad | points | stats] per step in flight; with N > 1 two
     # of them, so step k+1 searches while step k's buffer is gathered (NCCL, comm stream)
     nbuf = 2 if ws > 1 else 1
-    flats = [mdist.alloc_flat(n, cfg.nb, dev) for _ in range(nbuf)]
-    views = [mdist.flat_views(f, n, cfg.nb) for f in flats]
-    outs = [mdist.alloc_flat(n, cfg.nb, dev, ws) for _ in range(nbuf)] if ws > 1 else None
+    # N > 1: the search writes the 6-byte transport record (me_dcds_batch_packed: int8 MV,
+    # 16-bit SAD and NSP), 40% fewer bytes to gather than the 10-byte arrays
+    packed = ws > 1
+    flats = [mdist.alloc_flat(n, cfg.nb, dev, packed=packed) for _ in range(nbuf)]
+    views = [mdist.flat_views(f, n, cfg.nb, packed) for f in flats]
+    outs = [mdist.alloc_flat(n, cfg.nb, dev, ws, packed) for _ in range(nbuf)] if ws > 1 else None
     # high priority: the gather's NCCL blocks get SM slots as soon as search CTAs retire,
     # instead of waiting for the (many-wave) search grid to drain
     comm = torch.cuda.Stream(dev, priority=-1) if ws > 1 else None
@@ -336,7 +339,7 @@ def main():
         return b
 
     def search(b):
-        me.me_dcds_batch(frames, cfg.B, cfg.p, *views[b])
+        (me.me_dcds_batch_packed if packed else me.me_dcds_batch)(frames, cfg.B, cfg.p, *views[b])
         return b
 
     def gather(b):
@@ -378,7 +381,7 @@ def main():
         clk.mark_end()
     mv, sad, pts, st = views[(args.steps - 1) % nbuf]
     if ws > 1:  # the gathered copy of this rank's fields is its own output
-        mine = mdist.unpack_gathered(outs[(args.steps - 1) % nbuf], n, cfg.nb)[rank]
+        mine = mdist.unpack_gathered(outs[(args.steps - 1) % nbuf], n, cfg.nb, packed)[rank]
         assert torch.equal(mine[0], mv) and torch.equal(mine[3], st)
     launches = me.me_launch_count() - launches0
     total_ms = t_start.elapsed_time(t_end)
@@ -499,7 +502,7 @@ def main():
             t = torch.tensor([e2e_s], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        assert np.array_equal(hout[0].numpy(), mv.cpu().numpy())
+        assert np.array_equal(hout[0].numpy(), mv.cpu().numpy().astype(np.int16))
         line["e2e"] = {"value": ws * n * cfg.nb / e2e_s, "unit": UNIT,
                        "h2d_bytes_per_step": int(ws * in_bytes),
                        "d2h_bytes_per_step": int(ws * n * (cfg.nb * 10 + 24)),

@@ -88,6 +88,15 @@ int me_dcds_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride,
                   int W, int H, int block, int p, int16_t* mv_out, uint32_t* sad_out,
                   uint16_t* points_out, uint64_t* stats_out);
 
+/* me_dcds_batch with the outputs in the 6-byte transport record of the multi-GPU gather
+ * (SURVEY 8(e)): mv_out [npairs][nb][2] int8 (dx, dy; |d| <= p <= 32), sad_out [npairs][nb]
+ * uint16 (SAD <= 255 * 256), points_out [npairs][nb] uint16 -- the same values as
+ * me_dcds_batch's, 40% fewer bytes; stats_out as me_dcds_batch.  Outputs 2-byte aligned
+ * (stats 8-byte), else ME_EALIGN; other errors as me_dcds_batch. */
+int me_dcds_batch_packed(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                         int W, int H, int block, int p, int8_t* mv_out, uint16_t* sad_out,
+                         uint16_t* points_out, uint64_t* stats_out);
+
 /* DCDS^S (Table X): as me_dcds_batch but Step 4 scores only the middle point on the
  * side of the cheaper distant point of the final pattern (an infeasible distant point costs
  * +inf; a tie picks the negative side -- reading C22). */

@@ -64,6 +64,7 @@ struct SearchArgs {
     uint32_t* mv;           // [npairs][nb] packed (dx & 0xffff) | (dy << 16)
     uint32_t* sad;          // [npairs][nb]
     uint16_t* pts;          // [npairs][nb]
+    int packed;             // mv as int8 pairs [npairs][nb][2], sad as uint16 (me_dcds_batch_packed)
     unsigned long long* stats;  // [npairs][3] or null
     uint64_t* trace;            // TRACE builds: [npairs][nb][tcap] pass records
     uint16_t* tlen;             // TRACE builds: [npairs][nb] passes of each block
@@ -599,8 +600,13 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
     auto output = [&](uint32_t ss) {
         int cx, cy;
         gs.centre(p, cx, cy);
-        a.mv[gblk] = (uint32_t)(cx & 0xffff) | ((uint32_t)cy << 16);
-        a.sad[gblk] = gs.best;
+        if (a.packed) {  // 6-byte records: int8 (dx, dy), 16-bit SAD (<= 255*256), NSP
+            reinterpret_cast<uint16_t*>(a.mv)[gblk] = (uint16_t)((cx & 0xff) | ((cy & 0xff) << 8));
+            reinterpret_cast<uint16_t*>(a.sad)[gblk] = (uint16_t)gs.best;
+        } else {
+            a.mv[gblk] = (uint32_t)(cx & 0xffff) | ((uint32_t)cy << 16);
+            a.sad[gblk] = gs.best;
+        }
         a.pts[gblk] = (uint16_t)gs.pts;
         if (TRACE) a.tlen[gblk] = (uint16_t)gs.npass;
         acc_pts += (unsigned)gs.pts;

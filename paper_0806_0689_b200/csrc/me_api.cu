@@ -238,12 +238,13 @@ void launch_dcds_trace(const DcdsLaunch& L, int variant, const CUtensorMap& tc, 
 int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W, int H,
              int block, int p, int16_t* mv, uint32_t* sad, uint16_t* pts, uint64_t* stats,
              int variant, cudaStream_t s, uint64_t* trace = nullptr, uint16_t* tlen = nullptr,
-             int tcap = 0) {
+             int tcap = 0, bool packed = false) {
     DcdsLaunch L = plan_dcds(W, H, block, p, npairs);
     if ((int)L.smem > g_smem_optin) return fail(ME_EINVAL, "tile does not fit in shared memory");
     if (trace && !(L.G == (block == 16 ? 8 : 2) && L.NW == (block == 16 ? 8 : 4)))
         return fail(ME_EINVAL, "trace builds exist for the default lane-group geometry only (unset ME_G/ME_NW)");
     L.a.trace = trace; L.a.tlen = tlen; L.a.tcap = tcap;
+    L.a.packed = packed ? 1 : 0;
     L.a.cur0 = cur0; L.a.ref0 = ref0; L.a.stride = stride;
     L.a.mv = reinterpret_cast<uint32_t*>(mv);
     L.a.sad = sad;
@@ -531,6 +532,22 @@ int me_dcds_s_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_strid
     if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
     return run_dcds(cur0, ref0, pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out,
                     stats_out, 1, g_stream);
+}
+
+int me_dcds_batch_packed(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride, int npairs,
+                         int W, int H, int block, int p, int8_t* mv_out, uint16_t* sad_out,
+                         uint16_t* points_out, uint64_t* stats_out) {
+    int rc = validate_frames(cur0, ref0, pair_stride, npairs, W, H, block);
+    if (rc) return rc;
+    if (p < 1 || p > 32) return fail(ME_EINVAL, "p must be in [1, 32]");
+    if (!mv_out || !sad_out || !points_out) return fail(ME_EINVAL, "NULL output pointer");
+    if (!aligned(mv_out, 2) || !aligned(sad_out, 2) || !aligned(points_out, 2))
+        return fail(ME_EALIGN, "packed outputs must be 2-byte aligned");
+    if (stats_out && !aligned(stats_out, 8)) return fail(ME_EALIGN, "stats_out must be 8-byte aligned");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    return run_dcds(cur0, ref0, pair_stride, npairs, W, H, block, p,
+                    reinterpret_cast<int16_t*>(mv_out), reinterpret_cast<uint32_t*>(sad_out), points_out,
+                    stats_out, 0, g_stream, nullptr, nullptr, 0, true);
 }
 
 int me_dcds_trace_batch(int variant, const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride,

@@ -82,32 +82,39 @@ def gather_fields(mv, sad, pts, stats, npairs_total: int, group=None):
 # [mv | sad | points | stats], so the gather sends it as-is and the gathered result is unpacked
 # by views -- no packing copies on the step's critical path (bench.py, N > 1).
 # ---------------------------------------------------------------------------------------
-def flat_layout(n: int, nb: int):
+def flat_layout(n: int, nb: int, packed: bool = False):
     """Byte offsets and total size of the flat output buffer of n pairs x nb blocks:
-    mv [n, nb, 2] int16 | sad [n, nb] int32 | points [n, nb] int16 | stats [n, 3] int64
-    (stats 8-byte aligned; every part meets the C ABI's alignment)."""
+    mv [n, nb, 2] int16 | sad [n, nb] int32 | points [n, nb] int16 | stats [n, 3] int64, or with
+    packed=True the 6-byte transport record of me_dcds_batch_packed: mv [n, nb, 2] int8 | sad
+    [n, nb] uint16 | points [n, nb] uint16 | stats (stats 8-byte aligned; every part meets the C
+    ABI's alignment)."""
+    w_mv, w_sad = (2, 2) if packed else (4, 4)
     o_mv = 0
-    o_sad = o_mv + 4 * n * nb
-    o_pts = o_sad + 4 * n * nb
+    o_sad = o_mv + w_mv * n * nb
+    o_pts = o_sad + w_sad * n * nb
     o_st = (o_pts + 2 * n * nb + 7) & ~7
     total = o_st + 24 * n
     return o_mv, o_sad, o_pts, o_st, total
 
 
-def flat_views(buf: torch.Tensor, n: int, nb: int):
+def flat_views(buf: torch.Tensor, n: int, nb: int, packed: bool = False):
     """(mv, sad, points, stats) views of a flat uint8 buffer laid out by flat_layout."""
-    o_mv, o_sad, o_pts, o_st, total = flat_layout(n, nb)
+    o_mv, o_sad, o_pts, o_st, total = flat_layout(n, nb, packed)
     assert buf.dtype == torch.uint8 and buf.numel() >= total
-    mv = buf[o_mv:o_sad].view(torch.int16).view(n, nb, 2)
-    sad = buf[o_sad:o_pts].view(torch.int32).view(n, nb)
+    if packed:
+        mv = buf[o_mv:o_sad].view(torch.int8).view(n, nb, 2)
+        sad = buf[o_sad:o_pts].view(torch.int16).view(n, nb)
+    else:
+        mv = buf[o_mv:o_sad].view(torch.int16).view(n, nb, 2)
+        sad = buf[o_sad:o_pts].view(torch.int32).view(n, nb)
     pts = buf[o_pts:o_pts + 2 * n * nb].view(torch.int16).view(n, nb)
     st = buf[o_st:o_st + 24 * n].view(torch.int64).view(n, 3)
     return mv, sad, pts, st
 
 
-def alloc_flat(n: int, nb: int, device, world: int = 1):
+def alloc_flat(n: int, nb: int, device, world: int = 1, packed: bool = False):
     """A flat output buffer, or the [world, size] receive buffer of its gather."""
-    total = flat_layout(n, nb)[4]
+    total = flat_layout(n, nb, packed)[4]
     return torch.empty((world, total) if world > 1 else total, dtype=torch.uint8, device=device)
 
 
@@ -120,7 +127,7 @@ def gather_flat(buf: torch.Tensor, out: torch.Tensor, group=None):
     return out
 
 
-def unpack_gathered(out: torch.Tensor, n: int, nb: int):
+def unpack_gathered(out: torch.Tensor, n: int, nb: int, packed: bool = False):
     """Per-rank (mv, sad, points, stats) views of a gathered [world, size] buffer; rank r's
     pairs are the global pairs r*n .. r*n+n-1 (weak scaling: every rank searches n pairs)."""
-    return [flat_views(out[r], n, nb) for r in range(out.shape[0])]
+    return [flat_views(out[r], n, nb, packed) for r in range(out.shape[0])]

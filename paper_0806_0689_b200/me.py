@@ -22,7 +22,7 @@ SYMBOLS = (
     "me_init", "me_set_stream", "me_dcds", "me_fullsearch", "me_mc_psnr", "me_dcds_batch",
     "me_dcds_s_batch", "me_fullsearch_batch", "me_mc_sse_batch", "me_dcds_batch_host",
     "me_launch_count", "me_strerror", "me_shutdown", "me_quality_batch", "me_bma_batch",
-    "me_ideal_nsp_map", "me_mv_hist", "me_dcds_trace_batch",
+    "me_ideal_nsp_map", "me_mv_hist", "me_dcds_trace_batch", "me_dcds_batch_packed",
 )
 
 # me_alg ids (include/me.h)
@@ -57,6 +57,7 @@ def load() -> ctypes.CDLL:
                              ctypes.POINTER(ctypes.c_uint64)]
     L.me_dcds_batch.argtypes = batch
     L.me_dcds_s_batch.argtypes = batch
+    L.me_dcds_batch_packed.argtypes = batch
     L.me_fullsearch_batch.argtypes = batch
     L.me_dcds_batch_host.argtypes = batch
     L.me_mc_sse_batch.argtypes = [vp, vp, i64, i32, i32, i32, i32, vp, vp]
@@ -155,6 +156,12 @@ def _batch(fn, frames, block, p, mv, sad, pts, stats):
 
 def me_dcds_batch(frames, block, p, mv, sad, pts, stats=None):
     _batch(load().me_dcds_batch, frames, block, p, mv, sad, pts, stats)
+
+
+def me_dcds_batch_packed(frames, block, p, mv, sad, pts, stats=None):
+    """me_dcds_batch into the 6-byte transport record: mv [n, nb, 2] int8, sad [n, nb] int16
+    (holding uint16), pts [n, nb] int16 (holding uint16), stats [n, 3] int64."""
+    _batch(load().me_dcds_batch_packed, frames, block, p, mv, sad, pts, stats)
 
 
 def me_dcds_s_batch(frames, block, p, mv, sad, pts, stats=None):

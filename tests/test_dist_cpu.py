@@ -98,23 +98,28 @@ def test_gloo_gather_matches_single_rank(world, npairs):
         np.testing.assert_array_equal(a, b)
 
 
-def _flat_worker(rank, world, port, frames, B, p, out_q):
+def _flat_worker(rank, world, port, frames, B, p, out_q, packed=False):
     """Weak-scaling layout of bench.py: every rank searches its own n pairs into one flat
-    buffer and the buffers are all_gathered as they are."""
+    buffer (the 10-byte arrays, or with packed=True the 6-byte transport record) and the
+    buffers are all_gathered as they are."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     n = frames.shape[0] // world
     nb = (frames.shape[3] // B) * (frames.shape[2] // B)
-    buf = mdist.alloc_flat(n, nb, "cpu")
-    mv, sad, pts, st = mdist.flat_views(buf, n, nb)
+    buf = mdist.alloc_flat(n, nb, "cpu", packed=packed)
+    mv, sad, pts, st = mdist.flat_views(buf, n, nb, packed)
     omv, osad, opts, ost = _oracle_fields(frames[rank * n:(rank + 1) * n], B, p)
-    mv.copy_(omv); sad.copy_(osad); pts.copy_(opts); st.copy_(ost)
-    out = mdist.alloc_flat(n, nb, "cpu", world)
+    mv.copy_(omv.to(mv.dtype)); sad.copy_(osad.to(sad.dtype)); pts.copy_(opts); st.copy_(ost)
+    out = mdist.alloc_flat(n, nb, "cpu", world, packed)
     mdist.gather_flat(buf, out)
     if rank == 0:
-        parts = mdist.unpack_gathered(out, n, nb)
-        out_q.put([torch.cat([pr[k] for pr in parts]).numpy() for k in range(4)])
+        parts = mdist.unpack_gathered(out, n, nb, packed)
+        got = [torch.cat([pr[k] for pr in parts]) for k in range(4)]
+        if packed:  # back to the arrays' types (int8 MV, uint16 SAD)
+            got[0] = got[0].to(torch.int16)
+            got[1] = got[1].to(torch.int32) & 0xFFFF
+        out_q.put([t.numpy() for t in got])
     dist.barrier()
     dist.destroy_process_group()
 
@@ -123,16 +128,20 @@ def test_flat_layout_alignment():
     for n, nb in [(1, 99), (3, 7), (239, 32640)]:
         o_mv, o_sad, o_pts, o_st, total = mdist.flat_layout(n, nb)
         assert o_sad % 4 == 0 and o_pts % 2 == 0 and o_st % 8 == 0 and total >= o_st + 24 * n
+        o_mv, o_sad, o_pts, o_st, ptotal = mdist.flat_layout(n, nb, packed=True)
+        assert o_sad % 2 == 0 and o_pts % 2 == 0 and o_st % 8 == 0 and ptotal >= o_st + 24 * n
+        assert ptotal < total and o_st - 6 * n * nb < 8   # 6 bytes per block
 
 
-def test_gloo_flat_gather_matches_single_rank():
+@pytest.mark.parametrize("packed", [False, True])
+def test_gloo_flat_gather_matches_single_rank(packed):
     world, n = 2, 2
     cfg = synth.CONFIGS["c1"]
     frames = synth.make_sequence(cfg, pairs=range(1, world * n + 1)).numpy()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_flat_worker, args=(r, world, port, frames, cfg.B, cfg.p, q))
+    procs = [ctx.Process(target=_flat_worker, args=(r, world, port, frames, cfg.B, cfg.p, q, packed))
              for r in range(world)]
     for pr in procs:
         pr.start()

@@ -103,3 +103,25 @@ def test_bench_shapes_with_handout(knobs, B, p):
     got = run(fr, B, p, 0)
     for a, b in zip(ref, got):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_packed_record_equals_arrays(knobs, name):
+    """me_dcds_batch_packed (the 6-byte transport record of the multi-GPU gather) holds the
+    same values as me_dcds_batch: int8 MV, 16-bit SAD and NSP, identical stats."""
+    for k in KNOBS:
+        knobs.pop(k, None)
+    cfg = synth.CONFIGS[name]
+    fr = synth.make_sequence(cfg, device=DEV, pairs=[1, 5, 9])
+    n = fr.shape[0]
+    mv, sad, pts, st = me.alloc_outputs(n, cfg.nb, DEV)
+    me.me_dcds_batch(fr, cfg.B, cfg.p, mv, sad, pts, st)
+    pmv = torch.empty(n, cfg.nb, 2, dtype=torch.int8, device=DEV)
+    psad = torch.empty(n, cfg.nb, dtype=torch.int16, device=DEV)
+    ppts = torch.empty(n, cfg.nb, dtype=torch.int16, device=DEV)
+    pst = torch.empty(n, 3, dtype=torch.int64, device=DEV)
+    me.me_dcds_batch_packed(fr, cfg.B, cfg.p, pmv, psad, ppts, pst)
+    torch.cuda.synchronize()
+    assert torch.equal(pmv.to(torch.int16), mv)
+    assert torch.equal(psad.to(torch.int32) & 0xFFFF, sad)
+    assert torch.equal(ppts, pts) and torch.equal(pst, st)
