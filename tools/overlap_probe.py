@@ -1,7 +1,8 @@
 """One-GPU probe of the multi-GPU step's overlap (bench.py --gpus N): the DCDS search on the
 main stream while a communication-like kernel (a fixed number of CTAs streaming the bytes a
-rank receives in an 8-GPU all_gather of the c3 outputs, 7 x 78 MB) runs on a high-priority
-stream, as NCCL's kernels do.  Prints ms per step alone and with the concurrent copy."""
+rank receives in an 8-GPU all_gather of the c3 outputs: 7 x 47 MB as the 6-byte record,
+PROBE_RECORD=10 for the 10-byte arrays) runs on a high-priority stream, as NCCL's kernels do.
+Prints ms per step alone and with the concurrent copy."""
 import ctypes
 import os
 import subprocess
@@ -26,7 +27,8 @@ me.me_set_stream(main)
 cfg = synth.CONFIGS["c3"]
 fr = synth.make_sequence(cfg, device="cuda")
 outs = me.alloc_outputs(cfg.npairs, cfg.nb, "cuda")
-nbytes = 7 * cfg.npairs * (cfg.nb * 10 + 24)
+rec = int(os.environ.get("PROBE_RECORD", "6"))  # bytes per block: 6 (packed) or 10 (arrays)
+nbytes = 7 * cfg.npairs * (cfg.nb * rec + 24)
 src = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
 dst = torch.empty_like(src)
 comm = torch.cuda.Stream(priority=-1)
