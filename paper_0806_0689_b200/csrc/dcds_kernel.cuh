@@ -287,14 +287,23 @@ struct GroupState {
 
     // Pattern steps of pid (ids above): HDSP d0 (2,0) d1 (0,1); VDSP (1,0) (0,2); middle points
     // (1,0) / (0,1); DCDS^S distant points (2,0) / (0,2).
-    __device__ __forceinline__ void set_pattern(int np, int pitch, int bw) {
-        pid = np;
-        const bool v0 = (np == 5 || np == 7);                       // d0 vertical
-        const int a0 = (np == 2 || np == 6 || np == 7) ? 2 : 1;      // |d0|
-        db0 = v0 ? a0 * pitch : a0;
-        de0 = v0 ? a0 * bw : a0;
-        db1 = (np == 3 ? 2 : 1) * pitch;
-        de1 = (np == 3 ? 2 : 1) * bw;
+    // (kind 0 = horizontal, 1 = vertical; each setter is a few selects)
+    __device__ __forceinline__ void set_ddsp(int k, int pitch, int bw) {  // HDSP / VDSP
+        pid = 2 + k;
+        db0 = k ? 1 : 2;
+        de0 = db0;
+        db1 = k ? 2 * pitch : pitch;
+        de1 = k ? 2 * bw : bw;
+    }
+    __device__ __forceinline__ void set_middle(int k, int pitch, int bw) {  // Step 4
+        pid = 4 + k;
+        db0 = k ? pitch : 1;
+        de0 = k ? bw : 1;
+    }
+    __device__ __forceinline__ void set_distant(int k, int pitch, int bw) {  // DCDS^S look-up
+        pid = 6 + k;
+        db0 = k ? 2 * pitch : 2;
+        de0 = k ? 2 * bw : 2;
     }
 
     // Load the lane's current rows of the block at `crow0` (row stride `cpitch`).
@@ -377,7 +386,7 @@ struct GroupState {
             cidx += cy * bw + cx;
             kind = (cy == 0) ? 0 : 1;  // switching strategy one
             st = ST_S3; want = 0xf;
-            set_pattern(2 + kind, pitch, bw);
+            set_ddsp(kind, pitch, bw);
         }
     }
 
@@ -472,20 +481,21 @@ struct GroupState {
             if ((key >> 2) < best) {
                 best = key >> 2;
                 move(kb);
-                if ((kb >= 2) != (kind == 1)) { kind ^= 1; set_pattern(pid ^ 1, pitch, bm_row(p)); }  // near point
+                if ((kb >= 2) != (kind == 1)) { kind ^= 1; set_ddsp(kind, pitch, bm_row(p)); }  // near point
             } else {
                 st = VARIANT ? ST_S4PRE : ST_S4;  // BMP at the centre -> Step 4
-                set_pattern((VARIANT ? 6 : 4) + kind, pitch, bm_row(p));
+                if (VARIANT) set_distant(kind, pitch, bm_row(p));
+                else set_middle(kind, pitch, bm_row(p));
                 want = 3;
             }
-        } else if (st == ST_S4PRE) {
+        } else if (VARIANT && st == ST_S4PRE) {
             // DCDS^S: keep only the middle point beside the cheaper distant point;
             // an infeasible distant point costs +inf, ties go to the negative side (C22)
             const uint32_t dn = (m4 & 1) ? (v01 & 0xffffu) : 0xffffffffu;
             const uint32_t dp = (m4 & 2) ? (v01 >> 16) : 0xffffffffu;
             want = (dp < dn) ? 2 : 1;
             st = ST_S4;
-            set_pattern(4 + kind, pitch, bm_row(p));
+            set_middle(kind, pitch, bm_row(p));
         } else if (st == ST_S4) {
             // Step 4: strict minimum of the middle points against the centre
             if ((key >> 2) < best) {
