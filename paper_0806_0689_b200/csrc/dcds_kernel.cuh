@@ -12,18 +12,19 @@
 // C7); each position scored once per block (C5); window-only feasibility with an
 // edge-replicated reference (C8, C9); integer SAD (C12).
 //
-// Design (DESIGN.md "Kernels"): one CTA per tile of TBX x TBY blocks of one pair; the tile's
+// Design (DESIGN.md section 7): one CTA per tile of TBX x TBY blocks of one pair; the tile's
 // reference region (tile + the whole +-p window, edge-replicated) and current tile are staged
-// once into shared memory.  Each warp is split into 32/G lane groups; each group runs DCDS
-// on one block at a time (G lanes split the block's rows), so a warp carries 32/G blocks.
-// The search is a per-group state machine (S1a, S1b = the 7 HCSP points in two passes of 4
-// slots; S3 = the 4 DDSP points; S4 = the middle points) advanced one pass per warp
-// iteration, so groups at different steps share one instruction stream and the
-// data-dependent step count never needs a block or grid sync.  A group that finishes takes
-// the next block of the tile from a shared counter.  SADs use VABSDIFF4 (inline PTX
+// once into shared memory by TMA.  Each warp is split into 32/G lane groups (G lanes split a
+// block's rows).  In the default geometry (ONE) every group owns exactly one block of the
+// tile: it reads its current rows into registers, Step 1 runs as one straight-line step, and
+// Steps 2-4 are a per-group state machine (S3 = the 4 DDSP points, S4 = the middle points,
+// PRE = the DCDS^S look-up) advanced one pass per warp iteration, so groups at different
+// steps share one instruction stream and the data-dependent step count never needs a block
+// or grid sync; one dense phase after the warp's last search writes SSEs and outputs.  Other
+// tile shapes hand blocks out from a shared counter.  SADs use VABSDIFF4 (inline PTX
 // vabsdiff4.add) on funnel-shifted unaligned rows; the 4 slot sums are packed two per word
 // (each <= 255*B*B < 2^16) and reduced across the group with xor shuffles; argmins are
-// packed (SAD, order) keys; the visited set is a per-group bitmap in shared memory.
+// packed (SAD, order) keys; the visited set is a bordered per-group bitmap in shared memory.
 #pragma once
 #include <cuda.h>  // CUtensorMap
 #include <stdint.h>
