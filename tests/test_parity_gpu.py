@@ -377,10 +377,11 @@ def test_bma_ideal_mosaic_table7(B, alg, fixture):
     assert_pair_equal(np.stack([cur, ref]), B, 7, mv[0], sad[0], pts[0], alg, tag="mosaic")
 
 
-@pytest.mark.parametrize("alg", BMAS)
+@pytest.mark.parametrize("alg", BMAS + ["dcds_s"])
 def test_bma_c3_c4_sampled(alg):
     """Full-size frames, bench launch configuration (all pairs of a chunk in one launch),
-    checked on sampled blocks computed one by one by the oracle."""
+    checked on sampled blocks computed one by one by the oracle (DCDS^S included: the DCDS
+    kernels' VARIANT 1 at the bench shapes)."""
     rng = np.random.default_rng(17)
     for name, pairs in (("c3", [0, 57, 123]), ("c4", [0, 311])):
         cfg = synth.CONFIGS[name]
