@@ -17,6 +17,10 @@
  *   - Table VIII distribution 2, Table II weighted by the NSP map;
  *   - FS against an independent numpy brute force; zero-noise translations (closed form);
  *   - PSNR closed forms.
+ * Parity unpinned vs the paper (conventions where it is silent; pinned oracle<->GPU only):
+ * the order among the new points of a pattern (C7), the FS tie rule (C13) and DCDS^S's tie
+ * rule (C22); h-/v-HEXBS (C25) is pinned only weakly (Table VI pattern mass, zero-motion NSP
+ * 11, Table VIII distribution 2 within 0.1).
  */
 #include "oracle.h"
 
