@@ -427,6 +427,9 @@ def main():
         d = json.load(open(tp)).get(cfg.name)
         if d:
             roofline["traffic"] = d.get("dram_bytes_per_launch")
+            # what actually limits the kernel (same ncu capture): % of peak per resource
+            if d.get("limiters_pct"):
+                roofline["ncu_limiters_pct"] = d["limiters_pct"]
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
