@@ -83,14 +83,7 @@ __device__ __forceinline__ uint32_t ssd4(uint32_t a, uint32_t b, uint32_t c) {
     return __dp4a(d, d, c);
 }
 
-// 4 bytes starting at byte offset o of a 4-byte aligned shared buffer.
-__device__ __forceinline__ uint32_t lds_u8x4(const uint32_t* s, int o) {
-    const uint32_t lo = s[o >> 2], hi = s[(o >> 2) + 1];
-    return __funnelshift_r(lo, hi, (o & 3) << 3);
-}
 
-// Stage the reference region [ys, ys+rh) x [xs, xs+pitch) with edge replication, and the
-// current tile [y0, y0+TH) x [x0, x0+TW) (in-frame part), 16 bytes per thread-iteration.
 // ---- TMA / mbarrier helpers (sm_90+ PTX; SASS: UTMALDG, SYNCS.*) ---------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -229,7 +222,7 @@ __device__ __forceinline__ int hcsp_dy(int k) { return k < 5 ? 0 : (k == 5 ? -1 
 // (reading C8; pattern offsets are at most 2) reads as "already visited" and is neither
 // scored nor counted -- the test-and-set is the whole feasibility test.
 // ----------------------------------------------------------------------------------------
-enum : int { ST_DONE = 0, ST_S1A = 1, ST_S1B = 2, ST_S3 = 3, ST_S4 = 4, ST_S4PRE = 5, ST_IDLE = 6 };
+enum : int { ST_DONE = 0, ST_S1A = 1, ST_S3 = 3, ST_S4 = 4, ST_S4PRE = 5, ST_IDLE = 6 };
 
 // Visited-bitmap geometry for window +-p: row length, words.  The bitmaps of a CTA's groups
 // are interleaved: word w of group gi at bms[w * (groups + 4) + gi], so the groups' test-and-
