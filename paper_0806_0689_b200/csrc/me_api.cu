@@ -297,7 +297,10 @@ int run_bma(int alg, const uint8_t* cur0, const uint8_t* ref0, long long stride,
     const int ntx = (nbx + tbx - 1) / tbx, nty = (nby + tby - 1) / tby;
     const int TW = tbx * B, TH = tby * B;
     int pitch = ((TW + 2 * p + 31) + 15) & ~15;
-    if (((pitch >> 4) & 1) == 0) pitch += 16;
+    int p64 = pitch;  // the DCDS kernels' bank rule (plan_dcds)
+    while ((p64 & 127) != 64) p64 += 16;
+    if (B == 8 && p64 <= 256) pitch = p64;
+    else if (((pitch >> 4) & 1) == 0) pitch += 16;
     a.pitch = pitch;
     a.rh = TH + 2 * p;
     a.bm_words = me::bm_nwords(p);
