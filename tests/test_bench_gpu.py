@@ -45,3 +45,16 @@ def test_bench_json_contract():
     # value = blocks of all pairs / time per step
     cfg = d["config"]
     assert abs(d["value"] - cfg["pairs_per_gpu"] * cfg["blocks_per_pair"] / (d["ms_per_step"] * 1e-3)) < 1e-6 * d["value"]
+
+
+def test_bench_graph_mode_small_config():
+    """--graph: the timed steps replayed from one CUDA graph (small, launch-bound configs)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1", "--graph",
+                        "--steps", "20", "--warmup", "3", "--no-cmp", "--no-fs", "--no-e2e", "--no-cpu"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")][0])
+    assert d["config"]["cuda_graph"] is True and d["gpu_launches"] == 20 and d["value"] > 0
+    assert "L2-resident" in d["config"]["l2"]
