@@ -4,6 +4,7 @@ Each test names the PAPER.md passage (P:n) or the closed form / invariant / brut
 fixes the expected value.  None of the expected values comes from the CUDA path.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -381,3 +382,81 @@ def test_invalid_arguments():
         oracle.dcds(cur[:, :40], ref[:, :40], 16, 7)
     with pytest.raises(ValueError):
         oracle.dcds(cur, ref, 16, 0)
+
+
+# ---------------------------------------------------------------------------------------
+# DCDS^S side rule: "if the distortion on one distant point is smaller, the middle
+# point on the same side should more likely give the smaller distortion".  On the ideal
+# surface this rationale is exact wherever both distant points are in the window, so
+# the rule is pinned by placements where the two sides differ.
+# ---------------------------------------------------------------------------------------
+
+def _dcds_s_pin_failures(ideal_map):
+    """Failures of the DCDS^S side-rule pins for an ideal_nsp_map(p, variant) callable.
+
+    Hand traces (p = 7, cost = |q - t|; reading C22):
+    * t = (3,0): Step 1 -> (2,0) (cost 1); Step 2 HDSP@(2,0): (0,0) visited, (4,0) cost 1 ties
+      the centre (kept, C6), (2,+-1) cost sqrt 2 -> Step 4.  Distant points: (0,0) cost 3,
+      (4,0) cost 1 -> the cheaper is on the + side -> middle point (3,0) (new, cost 0):
+      MV (3,0), 7 + 3 + 1 = 11 points.  The reversed side would score (1,0), already visited in
+      Step 1: MV (2,0), 10 points.  t = (-3,0) mirrors it.
+    * t = (5,0): (2,0) -> (4,0) (distant, keep HDSP) -> HDSP@(4,0): (6,0) cost 1 ties -> Step 4
+      with distant (2,0) cost 3 vs (6,0) cost 1 -> (5,0): MV (5,0), 7 + 3 + 3 + 1 = 14.  The
+      reversed side scores (3,0) (new, cost 2): MV (4,0), 14 points.
+    * The miss set over the whole +-7 window: DCDS^S returns the true MV except where the
+      search ends one step inside the window edge on the long-wing axis, so the distant point
+      beyond the final centre is outside +-p (cost +inf, C22) and the middle point toward the
+      edge -- the true MV -- is never scored: t = (+-7,0) (final centre (+-6,0), HDSP) and
+      t = (x,+-7) for x in {+-3,+-5,+-7} (final centre (x,+-6), VDSP): exactly 14 placements.
+      (SURVEY C22 quoted 23 from a scratch script that is not available; every reading tried
+      -- tie to either side, infeasible distant point as +inf / check both / pick its side,
+      Euclidean / squared / L1 cost -- gives 14, 0 or 2, and the reversed rule 62.)"""
+    fails = []
+    nsp, mx, my = ideal_map(7, 1)
+    at = lambda tx, ty: (int(nsp[ty + 7, tx + 7]), (int(mx[ty + 7, tx + 7]), int(my[ty + 7, tx + 7])))
+    for t, want in [((3, 0), (11, (3, 0))), ((-3, 0), (11, (-3, 0))), ((5, 0), (14, (5, 0))),
+                    ((-5, 0), (14, (-5, 0)))]:
+        if at(*t) != want:
+            fails.append((t, at(*t), want))
+    ty, tx = np.mgrid[-7:8, -7:8]
+    miss = {(int(a), int(b)) for a, b in zip(tx[(mx != tx) | (my != ty)], ty[(mx != tx) | (my != ty)])}
+    expect = {(7, 0), (-7, 0)} | {(x, y) for x in (-7, -5, -3, 3, 5, 7) for y in (-7, 7)}
+    if miss != expect:
+        fails.append(("miss set", sorted(miss)))
+    return fails
+
+
+def test_dcds_s_side_rule_pins():
+    """P:417 side rule on the ideal surface (hand traces in _dcds_s_pin_failures)."""
+    assert _dcds_s_pin_failures(oracle.ideal_nsp_map) == []
+
+
+def test_dcds_s_pins_reject_reversed_side(tmp_path):
+    """Mutation check: the oracle compiled with the side rule reversed (middle point beside
+    the MORE expensive distant point) must fail the P:417 pins above."""
+    import ctypes
+    import subprocess
+    src = open(os.path.join(os.path.dirname(oracle.__file__), "oracle.c")).read()
+    good = "const int (*one)[2] = (dp < dn) ? mid + 1 : mid;"
+    assert src.count(good) == 1
+    mut = tmp_path / "oracle_mut.c"
+    mut.write_text(src.replace(good, "const int (*one)[2] = (dp < dn) ? mid : mid + 1;"))
+    so = tmp_path / "liboracle_mut.so"
+    subprocess.check_call(["gcc", *oracle.CFLAGS, "-I", os.path.dirname(oracle.__file__),
+                           "-o", str(so), str(mut), "-lm"])
+    L = ctypes.CDLL(str(so))
+    ip = ctypes.POINTER(ctypes.c_int)
+    L.oracle_ideal_nsp_map.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip, ip]
+
+    def mut_map(p, variant):
+        side = 2 * p + 1
+        bufs = [np.zeros(side * side, np.int32) for _ in range(3)]
+        assert L.oracle_ideal_nsp_map(p, variant, *[b.ctypes.data_as(ip) for b in bufs]) == 0
+        return [b.reshape(side, side) for b in bufs]
+
+    fails = _dcds_s_pin_failures(mut_map)
+    assert fails, "the reversed DCDS^S side rule passed the P:417 pins"
+    # the mutant's ideal-surface misses: 62 placements instead of 14
+    nsp, mx, my = mut_map(7, 1)
+    ty, tx = np.mgrid[-7:8, -7:8]
+    assert int(((mx != tx) | (my != ty)).sum()) == 62
