@@ -50,8 +50,10 @@ typedef enum {
     ME_ENOMEM = -5     /* device allocation failed (host-buffer variant only)             */
 } me_status;
 
-/* Select `device`, check it is sm_100 with enough shared memory, set kernel attributes.
- * Idempotent per device. */
+/* Select `device`, check it is sm_100 with enough shared memory, set kernel attributes,
+ * and allocate the library's device resources (scratch, copy streams, the staging buffers of
+ * me_dcds_batch_host).  Idempotent per device; calling it with another device first releases
+ * everything of the previous one (as me_shutdown), so no stream or buffer crosses devices. */
 int me_init(int device);
 
 /* cudaStream_t for every later launch (NULL = legacy default stream). */
@@ -188,11 +190,16 @@ int me_mc_sse_batch(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_strid
  * (MAD = sum SAD / (nb*B*B), MSE = SSE / (W*H), NSP = sum points / nb). */
 int me_quality_batch(const int16_t* mv, const int16_t* mv_fs, int npairs, int nb, double* out);
 
-/* End-to-end variant of me_dcds_batch on HOST buffers: frames (host, [npairs] x
- * pair_stride bytes as above) are copied to the device in chunks on two streams,
- * overlapped with the search of the previous chunk, and the outputs (host) copied back.
- * Synchronises.  Pinned host memory gives full copy bandwidth.  Returns ME_ENOMEM if the
- * staging buffers cannot be allocated. */
+/* End-to-end variant of me_dcds_batch on HOST buffers.  cur0, ref0: host, the frames of
+ * pair t at cur0 + t*pair_stride and ref0 + t*pair_stride (W*H bytes each; for npairs == 1
+ * pair_stride is ignored and cur / ref may be any two host buffers -- each frame is copied
+ * on its own, never the span between them).  Frames are copied to device staging buffers in
+ * chunks on two copy streams (cudaMemcpy2DAsync per chunk: cur rows, then ref rows), each
+ * chunk's search overlapping the next chunk's copy, and the outputs (host, as me_dcds_batch)
+ * copied back.  Synchronises, on success and on error: when it returns no copy touches the
+ * caller's buffers.  Pinned host memory gives full copy bandwidth.  The staging buffers are
+ * allocated by me_init (128 MiB of frames each); only a pair larger than that grows them,
+ * once (ME_ENOMEM if that fails).  No host pointer alignment is required. */
 int me_dcds_batch_host(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_stride,
                        int npairs, int W, int H, int block, int p, int16_t* mv_out,
                        uint32_t* sad_out, uint16_t* points_out, uint64_t* stats_out);

@@ -39,6 +39,10 @@ struct HostStage {
     size_t out_cap = 0;
 };
 HostStage g_stage[2];
+// frames per staging buffer of me_dcds_batch_host (allocated by me_init; a call whose single
+// pair exceeds it grows the buffers once)
+constexpr long long kStageFrames = 128ll << 20;
+cudaEvent_t g_order_ev = nullptr;  // orders the host-path copies after the library stream
 
 int set_cuda_err(cudaError_t e, const char* where) {
     snprintf(g_err, sizeof g_err, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
@@ -116,7 +120,8 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     int tby = (B == 16) ? 8 : 4;
     if (const char* e = getenv("ME_G")) {
         const int g = atoi(e);
-        if (g == 1 || g == 2 || g == 4 || g == 8) L.G = g;
+        // G = 1 (thread per block) is instantiated for 8x8 blocks only
+        if (g == 2 || g == 4 || g == 8 || (g == 1 && B == 8)) L.G = g;
     }
     if (const char* e = getenv("ME_TILE")) {
         int tx = 0, ty = 0;
@@ -448,6 +453,9 @@ extern "C" {
 
 int me_init(int device) {
     if (g_dev == device) return ME_OK;
+    // a different device: release the previous device's streams, scratch and staging first,
+    // so nothing of one device is used on another
+    if (g_dev >= 0) me_shutdown();
     int n = 0;
     CK(cudaGetDeviceCount(&n));
     if (device < 0 || device >= n) return fail(ME_EINVAL, "no such CUDA device");
@@ -502,6 +510,11 @@ int me_init(int device) {
     }
     for (auto& cs : g_copy_streams)
         if (!cs) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    if (!g_order_ev) CK(cudaEventCreateWithFlags(&g_order_ev, cudaEventDisableTiming));
+    for (auto& st : g_stage) {  // me_dcds_batch_host staging: allocated here, not per call
+        if ((rc = grow(&st.frames, &st.frames_cap, (size_t)kStageFrames))) return rc;
+        if ((rc = grow(&st.out, &st.out_cap, (size_t)kStageFrames / 4))) return rc;  // >= outputs of a full chunk
+    }
     g_dev = device;
     g_launches = 0;
     return ME_OK;
@@ -689,54 +702,60 @@ int me_dcds_batch_host(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_st
                        uint16_t* points_out, uint64_t* stats_out) {
     if (!cur0 || !ref0) return fail(ME_EINVAL, "NULL frame pointer");
     if (npairs > 1 && pair_stride < (long long)W * H) return fail(ME_EINVAL, "pair_stride smaller than a frame");
-    const long long span0 = std::llabs((long long)(ref0 - cur0)) + (long long)W * H;  // one pair
-    if (npairs > 1 && span0 > pair_stride) return fail(ME_EINVAL, "cur/ref of a pair must lie within pair_stride");
     // host pointers: alignment of the device staging copy is what the kernels need
     int rc = validate_search(reinterpret_cast<const uint8_t*>(16), reinterpret_cast<const uint8_t*>(16),
-                             pair_stride, npairs, W, H, block, p, mv_out, sad_out, points_out);
+                             16 * (((long long)W * H + 15) / 16), npairs, W, H, block, p, mv_out, sad_out,
+                             points_out);
     if (rc) return rc;
     if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
-    if ((std::llabs((long long)(ref0 - cur0)) & 15) != 0)
-        return fail(ME_EALIGN, "ref0 - cur0 must be a multiple of 16 bytes");
-    const uint8_t* hbase = std::min(cur0, ref0);
-    const long long cur_off = cur0 - hbase, ref_off = ref0 - hbase;
-    const long long stride = npairs > 1 ? pair_stride : ((span0 + 15) & ~15ll);
+    // device staging layout per chunk: [n][cur | ref], each frame W*H bytes, pair stride
+    // 2*W*H (a multiple of 16: W % 16 == 0).  cur and ref are copied separately, so the two
+    // host frames of a pair may be unrelated buffers.
+    const long long fsz = (long long)W * H, dstride = 2 * fsz;
+    const long long hstride = npairs > 1 ? pair_stride : fsz;  // host pitch (unused for one pair)
     const int nb = (W / block) * (H / block);
-    // chunk: ~256 MiB of frames per buffer
-    int chunk = (int)std::max(1ll, std::min<long long>(npairs, (256ll << 20) / stride));
-    const size_t fbytes = (size_t)stride * chunk;
+    const int chunk = (int)std::max(1ll, std::min<long long>(npairs, (long long)kStageFrames / dstride));
+    const size_t fbytes = (size_t)dstride * chunk;
     const size_t obytes = (size_t)chunk * nb * (4 + 4 + 2) + (size_t)chunk * 24 + 64;
-    for (auto& st : g_stage) {
+    for (auto& st : g_stage) {  // pre-allocated by me_init; grows only for frames > kStageFrames
         if ((rc = grow(&st.frames, &st.frames_cap, fbytes))) return rc;
         if ((rc = grow(&st.out, &st.out_cap, obytes))) return rc;
     }
     // order the copies after whatever the caller queued on the library stream
-    cudaEvent_t ev;
-    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    CK(cudaEventRecord(ev, g_stream));
-    for (auto cs : g_copy_streams) CK(cudaStreamWaitEvent(cs, ev, 0));
-    CK(cudaEventDestroy(ev));
-    for (int c0 = 0, ci = 0; c0 < npairs; c0 += chunk, ci++) {
-        const int n = std::min(chunk, npairs - c0);
-        HostStage& st = g_stage[ci & 1];
-        cudaStream_t s = g_copy_streams[ci & 1];
-        const size_t bytes = (size_t)(n - 1) * stride + (size_t)span0;
-        CK(cudaMemcpyAsync(st.frames, hbase + (size_t)c0 * stride, bytes, cudaMemcpyHostToDevice, s));
-        int16_t* dmv = reinterpret_cast<int16_t*>(st.out);
-        uint32_t* dsad = reinterpret_cast<uint32_t*>(st.out + (size_t)n * nb * 4);
-        uint64_t* dst = reinterpret_cast<uint64_t*>(st.out + (((size_t)n * nb * 8 + 7) & ~(size_t)7));
-        uint16_t* dpts = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(dst) + (size_t)n * 24);
-        rc = run_dcds(st.frames + cur_off, st.frames + ref_off, stride, n, W, H, block, p, dmv,
-                      dsad, dpts, dst, 0, s);
-        if (rc) return rc;
-        CK(cudaMemcpyAsync(mv_out + (size_t)c0 * nb * 2, dmv, (size_t)n * nb * 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(sad_out + (size_t)c0 * nb, dsad, (size_t)n * nb * 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(points_out + (size_t)c0 * nb, dpts, (size_t)n * nb * 2, cudaMemcpyDeviceToHost, s));
-        if (stats_out)
-            CK(cudaMemcpyAsync(stats_out + (size_t)c0 * 3, dst, (size_t)n * 24, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(g_order_ev, g_stream));
+    for (auto cs : g_copy_streams) CK(cudaStreamWaitEvent(cs, g_order_ev, 0));
+    auto body = [&]() -> int {
+        for (int c0 = 0, ci = 0; c0 < npairs; c0 += chunk, ci++) {
+            const int n = std::min(chunk, npairs - c0);
+            HostStage& st = g_stage[ci & 1];
+            cudaStream_t s = g_copy_streams[ci & 1];
+            // n frames of W*H bytes at host pitch hstride -> device pitch 2*W*H
+            CK(cudaMemcpy2DAsync(st.frames, (size_t)dstride, cur0 + (size_t)c0 * hstride, (size_t)hstride,
+                                 (size_t)fsz, (size_t)n, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpy2DAsync(st.frames + fsz, (size_t)dstride, ref0 + (size_t)c0 * hstride, (size_t)hstride,
+                                 (size_t)fsz, (size_t)n, cudaMemcpyHostToDevice, s));
+            int16_t* dmv = reinterpret_cast<int16_t*>(st.out);
+            uint32_t* dsad = reinterpret_cast<uint32_t*>(st.out + (size_t)n * nb * 4);
+            uint64_t* dst = reinterpret_cast<uint64_t*>(st.out + (((size_t)n * nb * 8 + 7) & ~(size_t)7));
+            uint16_t* dpts = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(dst) + (size_t)n * 24);
+            int r = run_dcds(st.frames, st.frames + fsz, dstride, n, W, H, block, p, dmv, dsad, dpts, dst, 0, s);
+            if (r) return r;
+            CK(cudaMemcpyAsync(mv_out + (size_t)c0 * nb * 2, dmv, (size_t)n * nb * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(sad_out + (size_t)c0 * nb, dsad, (size_t)n * nb * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(points_out + (size_t)c0 * nb, dpts, (size_t)n * nb * 2, cudaMemcpyDeviceToHost, s));
+            if (stats_out)
+                CK(cudaMemcpyAsync(stats_out + (size_t)c0 * 3, dst, (size_t)n * 24, cudaMemcpyDeviceToHost, s));
+        }
+        return ME_OK;
+    };
+    rc = body();
+    // always drain both copy streams: on an error no copy may still be reading or writing the
+    // caller's buffers when this returns
+    for (auto cs : g_copy_streams) {
+        const cudaError_t e = cudaStreamSynchronize(cs);
+        if (e != cudaSuccess && rc == ME_OK) rc = set_cuda_err(e, "cudaStreamSynchronize(copy stream)");
     }
-    for (auto cs : g_copy_streams) CK(cudaStreamSynchronize(cs));
-    return ME_OK;
+    return rc;
 }
 
 int64_t me_launch_count(void) { return g_launches; }
@@ -766,6 +785,8 @@ void me_shutdown(void) {
         if (cs) cudaStreamDestroy(cs);
         cs = nullptr;
     }
+    if (g_order_ev) cudaEventDestroy(g_order_ev);
+    g_order_ev = nullptr;
     g_stream = nullptr;
     g_dev = -1;
 }

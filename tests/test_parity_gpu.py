@@ -257,6 +257,37 @@ def test_host_buffer_variant_matches_device():
     np.testing.assert_array_equal(hst.numpy().astype(np.uint64), st)
 
 
+def test_host_buffer_variant_unrelated_single_pair():
+    """me_dcds_batch_host with npairs == 1 and cur / ref in two unrelated host buffers (the
+    ABI copies each frame on its own, never the span between them), odd pointer
+    offsets, and a re-init cycle (me_shutdown + me_init re-allocates the staging)."""
+    import ctypes
+    cfg = synth.CONFIGS["c0"]
+    fr = synth.make_sequence(cfg, device=DEV).cpu().numpy()
+    # the two frames far apart and at odd byte offsets inside their buffers
+    bc = np.zeros(cfg.W * cfg.H + 7, np.uint8)
+    br = np.zeros(cfg.W * cfg.H + 3 + (1 << 20), np.uint8)
+    cur = bc[7:]
+    ref = br[3 + (1 << 20):]
+    cur[:] = fr[0, 0].ravel()
+    ref[:] = fr[0, 1].ravel()
+    omv, osad, opts = oracle.dcds(fr[0, 0], fr[0, 1], cfg.B, cfg.p)
+    for cycle in range(2):
+        if cycle:
+            me.load().me_shutdown()
+            me.me_init(0)
+            me.me_set_stream(torch.cuda.current_stream())
+        hmv, hsad, hpts, hst = me.alloc_outputs(1, cfg.nb, "cpu")
+        L = me.load()
+        rc = L.me_dcds_batch_host(cur.ctypes.data, ref.ctypes.data, 0, 1, cfg.W, cfg.H, cfg.B, cfg.p,
+                                  hmv.data_ptr(), hsad.data_ptr(), hpts.data_ptr(), hst.data_ptr())
+        assert rc == 0, L.me_strerror(rc)
+        np.testing.assert_array_equal(hmv[0].numpy(), omv)
+        np.testing.assert_array_equal(hsad[0].numpy().astype(np.uint32), osad)
+        np.testing.assert_array_equal(hpts[0].numpy().astype(np.uint16), opts)
+        assert int(hst[0, 0]) == int(opts.sum()) and int(hst[0, 1]) == int(osad.sum())
+
+
 def test_user_stream_and_launch_count():
     cfg = synth.CONFIGS["c1"]
     fr = synth.make_sequence(cfg, device=DEV, pairs=[1, 2])
