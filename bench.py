@@ -51,6 +51,13 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cmp", action="store_true", help="skip the comparison-BMA section")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU searches the config's whole sequence (per-GPU work fixed); "
+                         "strong: the sequence's pairs are sharded over the GPUs (ceil shards)")
+    ap.add_argument("--gather", default="root", choices=["root", "all"],
+                    help="N > 1: NCCL gather of the MV records to rank 0, or all_gather to every rank")
+    ap.add_argument("--no-other-scaling", action="store_true",
+                    help="N > 1: skip the second (other --scaling) measurement")
     ap.add_argument("--graph", action="store_true",
                     help="N=1: capture the K timed steps in one CUDA graph and replay it (small "
                          "configs c0-c2, whose launches are a few microseconds)")
@@ -85,6 +92,8 @@ class ClockSampler:
         self.t0 = self.t1 = None
 
     def __enter__(self):
+        if self.index < 0:  # not sampled
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
@@ -288,6 +297,97 @@ def run_reference(args):
 # ------------------------------------------------------------------------------------------
 # the B200 arm
 # ------------------------------------------------------------------------------------------
+def timed_run(args, cfg, me, mdist, dist, ws, rank, dev, stream, scaling, sample_clocks=True):
+    """W warm-up + K timed steps of the hot path on this rank.
+
+    scaling "weak": every rank searches its own cfg.npairs pairs; "strong": the configured
+    cfg.npairs pairs are split into contiguous shards (dist.rank_pairs), the last one short.
+    A step = me_dcds_batch (N = 1) or me_dcds_batch_packed into a flat buffer followed by the
+    NCCL gather of the MV fields + statistics (N > 1: gather-to-rank-0 or all_gather,
+    --gather), the gather of step k overlapping the search of step k+1 (dist.GatherStep).
+    Time: CUDA events on the launch stream between a barrier + synchronize on both sides,
+    max over ranks."""
+    mine = mdist.rank_pairs(cfg.npairs, ws, rank, scaling)
+    n = len(mine)
+    per = cfg.npairs if scaling == "weak" else mdist.shard_size(cfg.npairs, ws)
+    frames = (synth.make_sequence(cfg, device=dev, pairs=range(1 + mine.start, 1 + mine.stop)) if n else
+              torch.empty(0, 2, cfg.H, cfg.W, dtype=torch.uint8, device=dev))
+    packed = ws > 1  # the 6-byte transport record (me_dcds_batch_packed): 40% fewer bytes to gather
+    step = mdist.GatherStep(n, per, cfg.nb, dev, ws, rank, packed, args.gather, stream=stream)
+    search_fn = me.me_dcds_batch_packed if packed else me.me_dcds_batch
+
+    def search(mv, sad, pts, st):
+        search_fn(frames, cfg.B, cfg.p, mv, sad, pts, st)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index if sample_clocks else -1) as clk:  # warm-up also brings clocks up
+        for k in range(max(args.warmup, 0)):
+            step.step(k, search)
+        step.drain()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        launches0 = me.me_launch_count()
+        torch.cuda.synchronize()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        if args.graph and ws == 1:
+            # the K steps as one CUDA graph (captured on torch's capture stream, which the
+            # library launches on while capturing); one replay is the timed region
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                me.me_set_stream(torch.cuda.current_stream())
+                for k in range(args.steps):
+                    search(*step.local_views(0))
+            me.me_set_stream(stream)
+            launches0 = me.me_launch_count() - args.steps  # the captured launches
+            graph.replay()  # warm the graph
+            torch.cuda.synchronize()
+            clk.mark_start()
+            t_start.record(stream)
+            graph.replay()
+            t_end.record(stream)
+            torch.cuda.synchronize()
+            clk.mark_end()
+            ev = None
+        else:
+            clk.mark_start()
+            t_start.record(stream)
+            for k in range(args.steps):
+                b = step.claim(k)  # (a wait on the previous gather is not kernel time)
+                ev[k][0].record(stream)
+                if n:
+                    search(*step.local_views(b))
+                ev[k][1].record(stream)
+                step.collect(b)
+                step.last = b
+            step.drain()  # the last gathers are inside the timed region
+            t_end.record(stream)
+            torch.cuda.synchronize()
+            clk.mark_end()
+    launches = me.me_launch_count() - launches0
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev] if ev else [total_ms / args.steps] * args.steps
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    local = step.local_views(step.last)
+    pairs_all = ws * cfg.npairs if scaling == "weak" else cfg.npairs
+    out = {"n": n, "frames": frames, "total_ms": total_ms, "kern_ms": kern_ms, "launches": launches,
+           "clocks": clk.summary(), "local": local, "step": step, "pairs_all": pairs_all,
+           "value": pairs_all * cfg.nb / (total_ms / args.steps * 1e-3), "scaling": scaling}
+    if ws > 1:  # the gathered copy of this rank's pairs equals its own output
+        g = step.gathered(cfg.npairs, scaling)
+        if g is not None and n:
+            off = mine.start
+            assert torch.equal(g[0][off:off + n], local[0]) and torch.equal(g[3][off:off + n], local[3])
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -312,113 +412,16 @@ def main():
     me.me_set_stream(stream)
 
     cfg = synth.CONFIGS[args.config]
-    # weak scaling: every rank searches its own cfg.npairs pairs (pair indices offset by rank)
-    n = cfg.npairs
-    pairs = range(1 + rank * n, 1 + (rank + 1) * n)
-    frames = synth.make_sequence(cfg, device=dev, pairs=pairs)
-    in_bytes = frames.numel()
     from paper_0806_0689_b200 import dist as mdist
-    # outputs: one flat buffer [mv | sad | points | stats] per step in flight; with N > 1 two
-    # of them, so step k+1 searches while step k's buffer is gathered (NCCL, comm stream)
-    nbuf = 2 if ws > 1 else 1
-    # N > 1: the search writes the 6-byte transport record (me_dcds_batch_packed: int8 MV,
-    # 16-bit SAD and NSP), 40% fewer bytes to gather than the 10-byte arrays
-    packed = ws > 1
-    flats = [mdist.alloc_flat(n, cfg.nb, dev, packed=packed) for _ in range(nbuf)]
-    views = [mdist.flat_views(f, n, cfg.nb, packed) for f in flats]
-    outs = [mdist.alloc_flat(n, cfg.nb, dev, ws, packed) for _ in range(nbuf)] if ws > 1 else None
-    # high priority: the gather's NCCL blocks get SM slots as soon as search CTAs retire,
-    # instead of waiting for the (many-wave) search grid to drain
-    comm = torch.cuda.Stream(dev, priority=-1) if ws > 1 else None
-    ready = [torch.cuda.Event() for _ in range(nbuf)]
-    freed = [torch.cuda.Event() for _ in range(nbuf)]
-    used = [False] * nbuf
-    torch.cuda.synchronize()
-
-    def claim(k):
-        b = k % nbuf
-        if used[b]:
-            stream.wait_event(freed[b])  # the gather of this buffer's previous step is done
-        return b
-
-    def search(b):
-        (me.me_dcds_batch_packed if packed else me.me_dcds_batch)(frames, cfg.B, cfg.p, *views[b])
-        return b
-
-    def gather(b):
-        # NCCL all_gather of every rank's per-pair MV fields + statistics (the flat buffer as
-        # it is; paper_0806_0689_b200/dist.py) -- the path's only collective, overlapped with
-        # the next step's search
-        if ws > 1:
-            ready[b].record(stream)
-            comm.wait_event(ready[b])
-            with torch.cuda.stream(comm):
-                mdist.gather_flat(flats[b], outs[b])
-            freed[b].record(comm)
-            used[b] = True
-
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    with ClockSampler(local) as clk:  # started first: warm-up steps also bring clocks up
-        for k in range(max(args.warmup, 0)):
-            gather(search(claim(k)))
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        launches0 = me.me_launch_count()
-        torch.cuda.synchronize()
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        if args.graph and ws == 1:
-            # the K steps as one CUDA graph (captured on torch's capture stream, which the
-            # library launches on while capturing); one replay is the timed region
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                me.me_set_stream(torch.cuda.current_stream())
-                for k in range(args.steps):
-                    search(claim(k))
-            me.me_set_stream(stream)
-            launches0 = me.me_launch_count() - args.steps  # the captured launches
-            graph.replay()  # warm the graph
-            torch.cuda.synchronize()
-            clk.mark_start()
-            t_start.record(stream)
-            graph.replay()
-            t_end.record(stream)
-            torch.cuda.synchronize()
-            clk.mark_end()
-            ev = None
-        else:
-            clk.mark_start()
-            t_start.record(stream)
-            for k in range(args.steps):
-                b = claim(k)  # (a wait on the previous gather is not kernel time)
-                ev[k][0].record(stream)
-                search(b)
-                ev[k][1].record(stream)
-                gather(b)
-            if comm is not None:
-                stream.wait_stream(comm)  # the last gathers are inside the timed region
-            t_end.record(stream)
-            torch.cuda.synchronize()
-            clk.mark_end()
-    mv, sad, pts, st = views[(args.steps - 1) % nbuf]
-    if ws > 1:  # the gathered copy of this rank's fields is its own output
-        mine = mdist.unpack_gathered(outs[(args.steps - 1) % nbuf], n, cfg.nb, packed)[rank]
-        assert torch.equal(mine[0], mv) and torch.equal(mine[3], st)
-    launches = me.me_launch_count() - launches0
-    total_ms = t_start.elapsed_time(t_end)
-    kern_ms = [a.elapsed_time(b) for a, b in ev] if ev else [total_ms / args.steps] * args.steps
-    if ws > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        dist.barrier()
+    run = timed_run(args, cfg, me, mdist, dist, ws, rank, dev, stream, args.scaling)
+    mv, sad, pts, st = run["local"]
+    n, frames, total_ms, kern_ms, launches, clocks = (run["n"], run["frames"], run["total_ms"], run["kern_ms"],
+                                                     run["launches"], run["clocks"])
+    in_bytes = frames.numel()
     ms_per_step = total_ms / args.steps
     stats = st.cpu().numpy().astype(np.float64)
     sum_pts = float(stats[:, 0].sum())
-    blocks_per_step_rank = n * cfg.nb
-    value = ws * blocks_per_step_rank / (ms_per_step * 1e-3)
+    value = run["value"]
 
     # roofline of the dominant kernel (dcds_kernel), algorithmic bytes / ops per launch
     hbm_peak, hbm_src = load_peaks()
@@ -428,7 +431,6 @@ def main():
     achieved_gbs = alg_bytes / kern_avg_s / 1e9
     lane_ops = sum_pts * cfg.B * cfg.B / 4.0            # VABSDIFF4 lane-ops the method needs
     r_clk, sms = load_int_peak()
-    clocks = clk.summary()
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved_gbs / hbm_peak, "traffic": None, "peak_source": hbm_src,
                 "alg_bytes_per_launch": alg_bytes}
@@ -457,21 +459,24 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded; SURVEY 8(d) generator; paper's sequences unavailable)",
         "config": {
             "workload": f"{cfg.name}: {cfg.W}x{cfg.H} luma, {cfg.B}x{cfg.B} blocks, +-{cfg.p} window, "
-                        f"{n} frame pairs per GPU",
-            "pairs_per_gpu": n, "blocks_per_pair": cfg.nb, "W": cfg.W, "H": cfg.H,
-            "block": cfg.B, "p": cfg.p,
-            "frames_per_sec": ws * n / (ms_per_step * 1e-3),
+                        + (f"{cfg.npairs} frame pairs per GPU" if args.scaling == "weak" else
+                           f"{cfg.npairs} frame pairs sharded over {ws} GPU(s)"),
+            "pairs_per_gpu": n, "pairs_all_gpus": run["pairs_all"], "blocks_per_pair": cfg.nb,
+            "W": cfg.W, "H": cfg.H, "block": cfg.B, "p": cfg.p,
+            "frames_per_sec": run["pairs_all"] / (ms_per_step * 1e-3),
             "mean_nsp": sum_pts / (n * cfg.nb),
             "l2": (f"inputs {in_bytes / 2**20:.0f} MiB per GPU > 126 MB L2 (no flush needed)"
                    if in_bytes > 126e6 else
                    f"inputs {in_bytes / 2**20:.1f} MiB per GPU fit the 126 MB L2: L2-resident, not flushed "
                    "(a small parity config, not the bench line)"),
             "cuda_graph": bool(args.graph and ws == 1),
-            "parallelism": f"dp{ws} (frame pairs sharded; NCCL all_gather of MV fields + stats)"
+            "parallelism": (f"dp{ws} (frame pairs sharded; NCCL "
+                            + ("gather to rank 0" if args.gather == "root" else "all_gather")
+                            + " of the 6-byte MV records + stats, overlapped with the next search)")
                            if ws > 1 else "single GPU",
         },
         "gpu_launches": int(launches),
@@ -479,6 +484,16 @@ def main():
         "roofline": roofline,
         "clocks": clocks,
     }
+
+    if ws > 1 and not args.no_other_scaling:
+        # the other sharding of the same sequence, measured in the same run (the driver's
+        # scaling run compares per-N values of the main line)
+        other = "strong" if args.scaling == "weak" else "weak"
+        r2 = timed_run(args, cfg, me, mdist, dist, ws, rank, dev, stream, other, sample_clocks=False)
+        line["other_scaling"] = {"scaling": other, "value": r2["value"], "unit": UNIT,
+                                 "ms_per_step": r2["total_ms"] / args.steps,
+                                 "pairs_all_gpus": r2["pairs_all"], "pairs_per_gpu_rank0": r2["n"],
+                                 "kernel_ms_mean_rank0": statistics.mean(r2["kern_ms"])}
 
     if rank == 0 and not args.no_fs:
         # FS (quality reference), same pairs, small sample: timed beside the path
@@ -515,27 +530,31 @@ def main():
     if not args.no_e2e:
         # end to end through the C ABI on HOST buffers, on every rank: H2D of the frames
         # (pinned), search, D2H of the MV field + stats, every step; max over ranks
-        hfr = frames.cpu().pin_memory()
-        hout = [t.pin_memory() for t in me.alloc_outputs(n, cfg.nb, "cpu")]
-        me.me_dcds_batch_host(hfr, cfg.B, cfg.p, *hout)
+        e2e_s = 0.0
+        if n:
+            hfr = frames.cpu().pin_memory()
+            hout = [t.pin_memory() for t in me.alloc_outputs(n, cfg.nb, "cpu")]
+            me.me_dcds_batch_host(hfr, cfg.B, cfg.p, *hout)
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(args.e2e_steps):
-            me.me_dcds_batch_host(hfr, cfg.B, cfg.p, *hout)
-        b.record(stream)
-        torch.cuda.synchronize()
-        e2e_s = a.elapsed_time(b) * 1e-3 / args.e2e_steps
+        if n:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.e2e_steps):
+                me.me_dcds_batch_host(hfr, cfg.B, cfg.p, *hout)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e_s = a.elapsed_time(b) * 1e-3 / args.e2e_steps
+            assert np.array_equal(hout[0].numpy(), mv.cpu().numpy().astype(np.int16))
         if ws > 1:
             t = torch.tensor([e2e_s], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        assert np.array_equal(hout[0].numpy(), mv.cpu().numpy().astype(np.int16))
-        line["e2e"] = {"value": ws * n * cfg.nb / e2e_s, "unit": UNIT,
-                       "h2d_bytes_per_step": int(ws * in_bytes),
-                       "d2h_bytes_per_step": int(ws * n * (cfg.nb * 10 + 24)),
+        pa = run["pairs_all"]
+        line["e2e"] = {"value": pa * cfg.nb / e2e_s, "unit": UNIT,
+                       "h2d_bytes_per_step": int(pa * 2 * cfg.W * cfg.H),
+                       "d2h_bytes_per_step": int(pa * (cfg.nb * 10 + 24)),
                        "ms_per_step": e2e_s * 1e3, "steps": args.e2e_steps,
                        "note": "all ranks, each on its own pairs and PCIe link; max time over ranks"}
 

@@ -131,3 +131,113 @@ def unpack_gathered(out: torch.Tensor, n: int, nb: int, packed: bool = False):
     """Per-rank (mv, sad, points, stats) views of a gathered [world, size] buffer; rank r's
     pairs are the global pairs r*n .. r*n+n-1 (weak scaling: every rank searches n pairs)."""
     return [flat_views(out[r], n, nb, packed) for r in range(out.shape[0])]
+
+
+# ---------------------------------------------------------------------------------------
+# The multi-GPU step of bench.py (SURVEY 8(e)): search this rank's pairs into a flat buffer,
+# then gather the buffers of all ranks -- double-buffered, the gather of step k on a comm
+# stream overlapping the search of step k+1.
+# ---------------------------------------------------------------------------------------
+def rank_pairs(npairs: int, world: int, rank: int, scaling: str):
+    """Global pair indices (0-based) this rank searches.  weak: every rank its own npairs
+    pairs (rank r: r*npairs ..); strong: the configured npairs split in contiguous ceil
+    shards (shard), the last ones possibly short or empty."""
+    if scaling == "weak":
+        return range(rank * npairs, (rank + 1) * npairs)
+    lo, hi = shard(npairs, world, rank)
+    return range(lo, hi)
+
+
+class GatherStep:
+    """One step = search of this rank's pairs (search_fn(views) writes mv / sad / points /
+    stats into the views of a flat buffer of `per` pairs -- the padded shard size, so every
+    rank's buffer has the same size) + the collective over that buffer:
+      gather="all":  all_gather_into_tensor into [world, size] on every rank;
+      gather="root": gather to rank 0 (NCCL send/recv under torch.distributed.gather), the
+                     other ranks only send -- the north star's "gathered".
+    With world == 1 there is no collective.  Two flat buffers alternate: the search that
+    next writes a buffer waits on the event recorded after that buffer's last gather."""
+
+    def __init__(self, n_local: int, per: int, nb: int, device, world: int, rank: int,
+                 packed: bool, gather: str = "root", comm_stream=None, stream=None, nbuf=None,
+                 collective: bool | None = None):
+        assert gather in ("all", "root")
+        self.n, self.per, self.nb, self.world, self.rank = n_local, per, nb, world, rank
+        self.packed, self.gather = packed, gather
+        # world == 1 has nothing to gather; collective=True runs the NCCL call anyway (tests)
+        self.coll = world > 1 if collective is None else collective
+        self.nbuf = nbuf or (2 if self.coll else 1)
+        self.flats = [alloc_flat(per, nb, device, packed=packed) for _ in range(self.nbuf)]
+        for f in self.flats:
+            f.zero_()  # padding pairs of a short shard gather as zeros
+        self.views = [flat_views(f, per, nb, packed) for f in self.flats]
+        recv = self.coll and (gather == "all" or rank == 0)
+        self.outs = ([alloc_flat(per, nb, device, world, packed).view(world, -1) for _ in range(self.nbuf)]
+                     if recv else None)
+        # CPU (gloo tests): synchronous, no streams or events
+        self.cuda = torch.device(device).type == "cuda"
+        self.stream = self.comm = None
+        if self.cuda:
+            self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+            self.comm = comm_stream
+            if self.coll and self.comm is None:
+                # high priority: NCCL's blocks get SM slots as soon as search CTAs retire
+                self.comm = torch.cuda.Stream(device, priority=-1)
+        self.ready = [torch.cuda.Event() for _ in range(self.nbuf)] if self.cuda else None
+        self.freed = [torch.cuda.Event() for _ in range(self.nbuf)] if self.cuda else None
+        self.used = [False] * self.nbuf
+        self.last = 0
+
+    def local_views(self, b):
+        """this rank's n pairs of buffer b (the leading part of the padded buffer)"""
+        mv, sad, pts, st = self.views[b]
+        return mv[: self.n], sad[: self.n], pts[: self.n], st[: self.n]
+
+    def claim(self, k: int) -> int:
+        b = k % self.nbuf
+        if self.used[b] and self.cuda:
+            self.stream.wait_event(self.freed[b])
+        return b
+
+    def _collective(self, b: int):
+        if self.gather == "all":
+            gather_flat(self.flats[b], self.outs[b])
+        else:
+            gl = list(self.outs[b].unbind(0)) if self.rank == 0 else None
+            dist.gather(self.flats[b], gl, dst=0)
+
+    def collect(self, b: int):
+        if not self.coll:
+            return
+        if not self.cuda:
+            self._collective(b)
+            return
+        self.ready[b].record(self.stream)
+        self.comm.wait_event(self.ready[b])
+        with torch.cuda.stream(self.comm):
+            self._collective(b)
+        self.freed[b].record(self.comm)
+        self.used[b] = True
+
+    def step(self, k: int, search_fn):
+        b = self.claim(k)
+        if self.n:
+            search_fn(*self.local_views(b))
+        self.collect(b)
+        self.last = b
+        return b
+
+    def drain(self):
+        if self.cuda and self.comm is not None:
+            self.stream.wait_stream(self.comm)
+
+    def gathered(self, npairs_total: int, scaling: str):
+        """(mv, sad, points, stats) of all ranks' pairs in global pair order from the last
+        step's receive buffer (rank 0, or every rank with gather="all"); None elsewhere."""
+        if not self.coll:
+            return tuple(t.clone() for t in self.local_views(self.last))
+        if self.outs is None:
+            return None
+        parts = [flat_views(self.outs[self.last][r], self.per, self.nb, self.packed) for r in range(self.world)]
+        sizes = [len(rank_pairs(npairs_total, self.world, r, scaling)) for r in range(self.world)]
+        return tuple(torch.cat([pr[k][:s] for pr, s in zip(parts, sizes)]) for k in range(4))

@@ -152,3 +152,70 @@ def test_gloo_flat_gather_matches_single_rank(packed):
     ref = [t.numpy() for t in _oracle_fields(frames, cfg.B, cfg.p)]
     for a, b in zip(got, ref):
         np.testing.assert_array_equal(a, b)
+
+
+def _step_worker(rank, world, port, frames_all, B, p, out_q, scaling, gather, packed, npairs):
+    """bench.py's multi-GPU step (GatherStep) on gloo: this rank's pairs (weak or strong
+    sharding, rank_pairs) searched into the padded flat buffer (the oracle stands in for the
+    kernel), then all_gather / gather-to-root; rank 0 reassembles all pairs in order."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nb = (frames_all.shape[3] // B) * (frames_all.shape[2] // B)
+    mine = mdist.rank_pairs(npairs, world, rank, scaling)
+    per = npairs if scaling == "weak" else mdist.shard_size(npairs, world)
+    step = mdist.GatherStep(len(mine), per, nb, "cpu", world, rank, packed, gather)
+
+    def search(mv, sad, pts, st):
+        omv, osad, opts, ost = _oracle_fields(frames_all[mine.start:mine.stop], B, p)
+        mv.copy_(omv.to(mv.dtype)); sad.copy_(osad.to(sad.dtype)); pts.copy_(opts); st.copy_(ost)
+
+    for k in range(3):  # several steps: the buffers alternate
+        step.step(k, search)
+    step.drain()
+    g = step.gathered(npairs, scaling)
+    if rank == 0 or gather == "all":
+        got = list(g)
+        if packed:
+            got[0] = got[0].to(torch.int16)
+            got[1] = got[1].to(torch.int32) & 0xFFFF
+        if rank == 0:
+            out_q.put([t.numpy() for t in got])
+    else:
+        assert g is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scaling,gather,packed,npairs", [
+    ("strong", "root", True, 3),    # uneven shards: 2 + 1
+    ("strong", "all", False, 3),
+    ("strong", "root", False, 1),   # rank 1 has no pairs (empty shard)
+    ("weak", "root", True, 2),
+    ("weak", "all", True, 1),
+])
+def test_gloo_gather_step(scaling, gather, packed, npairs):
+    world = 2
+    cfg = synth.CONFIGS["c1"]
+    total = npairs * world if scaling == "weak" else npairs
+    frames = synth.make_sequence(cfg, pairs=range(1, total + 1)).numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, world, port, frames, cfg.B, cfg.p, q, scaling, gather,
+                                                    packed, npairs)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    ref = [t.numpy() for t in _oracle_fields(frames, cfg.B, cfg.p)]
+    for a, b in zip(got, ref):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_rank_pairs():
+    assert [list(mdist.rank_pairs(5, 2, r, "strong")) for r in range(2)] == [[0, 1, 2], [3, 4]]
+    assert [list(mdist.rank_pairs(3, 2, r, "weak")) for r in range(2)] == [[0, 1, 2], [3, 4, 5]]
+    assert list(mdist.rank_pairs(1, 4, 3, "strong")) == []
