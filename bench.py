@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cmp", action="store_true", help="skip the comparison-BMA section")
+    ap.add_argument("--no-mcsse", action="store_true", help="skip the standalone MC-SSE timing")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every GPU searches the config's whole sequence (per-GPU work fixed); "
@@ -455,6 +456,12 @@ def main():
             # what actually limits the kernel (same ncu capture): % of peak per resource
             if d.get("limiters_pct"):
                 roofline["ncu_limiters_pct"] = d["limiters_pct"]
+            # SURVEY 8(d) evidence of the same capture (tools/ncu_evidence.py): halo
+            # over-fetch L2 -> SM, executed / algorithmic VABSDIFF4 lane-ops, per-block budget
+            for k in ("l2_to_sm_over_alg", "vabsdiff4_exec_over_alg", "vabsdiff4_exec_over_alg_plus_fused_sse",
+                      "warp_inst_per_block", "smem_wavefronts_per_block", "source"):
+                if k in d:
+                    roofline["ncu_" + k] = d[k]
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -516,6 +523,31 @@ def main():
         if r_clk is not None:
             fsline["alu_frac"] = (fs_ops / fs_s) / roofline["int_peak_lane_ops_per_s"]
         line["fullsearch"] = fsline
+
+    if rank == 0 and not args.no_mcsse:
+        # the motion-compensated SSE (P:342 aspect 4) standalone over every pair at the DCDS MV
+        # field ("MC-PSNR fused and standalone"; fused it is part of the step)
+        mvf = mv if mv.dtype == torch.int16 else None
+        if mvf is None:
+            mvf = me.alloc_outputs(n, cfg.nb, dev)[0]
+            me.me_dcds_batch(frames, cfg.B, cfg.p, mvf, *me.alloc_outputs(n, cfg.nb, dev)[1:3])
+        sse = torch.empty(n, dtype=torch.int64, device=dev)
+        me.me_mc_sse_batch(frames, cfg.B, mvf, sse)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        a.record(stream)
+        for _ in range(reps):
+            me.me_mc_sse_batch(frames, cfg.B, mvf, sse)
+        b.record(stream)
+        torch.cuda.synchronize()
+        mc_s = a.elapsed_time(b) * 1e-3 / reps
+        if mv.dtype == torch.int16:  # equals the SSE the fused search reported
+            assert torch.equal(sse, st[:, 2]), "standalone MC-SSE != fused"
+        mc_bytes = n * (2 * cfg.W * cfg.H + 4 * cfg.nb + 8)
+        line["mc_sse_standalone"] = {"value": n * cfg.nb / mc_s, "unit": UNIT, "ms": mc_s * 1e3, "pairs": n,
+                                     "alg_bytes": mc_bytes, "achieved_gbs": mc_bytes / mc_s / 1e9,
+                                     "frac_hbm": mc_bytes / mc_s / 1e9 / hbm_peak}
 
     if rank == 0 and not args.no_cmp:
         # the paper's comparison (Table IX): every BMA on a

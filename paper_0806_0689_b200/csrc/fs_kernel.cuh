@@ -211,7 +211,15 @@ __global__ void __launch_bounds__(512)
     }
 }
 
-// Motion-compensated SSE: one warp per block, clamped reference reads (reading C9).
+// Motion-compensated SSE (P:342 aspect 4; reading C18): SSE = sum over the frame of
+// (cur - R(x + mvx, y + mvy))^2 with R the edge-replicated reference (reading C9).
+// HBM-bound: every frame byte is read once.  One lane per block row (B lanes per block, 32/B
+// blocks per warp): the current row is one aligned vector load (8 / 16 bytes: bx is a
+// multiple of B and W of 16), the reference row at the MV is B/4 + 1 aligned words funnel-
+// shifted to the row's byte offset, squared differences by VABSDIFF4 + IDP.4A.  Blocks whose
+// displaced block leaves the frame take the clamped byte path (border blocks only).  Per-CTA
+// sums (32-bit: at most 8 warps x 32 / B blocks x 65025 B^2 = 133 M (B = 8) / 266 M (B = 16)) are added to the
+// pair's u64 with one atomic per CTA.
 struct McArgs {
     const uint8_t* cur0;
     const uint8_t* ref0;
@@ -222,27 +230,73 @@ struct McArgs {
     unsigned long long* sse;
 };
 
+template <int B>
 __global__ void __launch_bounds__(256) mc_sse_kernel(const McArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int bi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    constexpr int BPW = 32 / B;            // blocks per warp
+    constexpr int W4 = B / 4;              // words per row
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int row = lane % B;
+    const int bi = (blockIdx.x * 8 + warp) * BPW + lane / B;
     const int pair = blockIdx.y;
-    if (bi >= a.nb) return;
     const uint8_t* cur = a.cur0 + (long long)pair * a.stride;
     const uint8_t* ref = a.ref0 + (long long)pair * a.stride;
-    const int B = a.B;
-    const int bx = (bi % a.nbx) * B, by = (bi / a.nbx) * B;
-    const uint32_t m = a.mv[(long long)pair * a.nb + bi];
-    const int dx = (int)(int16_t)(m & 0xffff), dy = (int)(int16_t)(m >> 16);
     uint32_t s = 0;
-    for (int e = lane; e < B * B; e += 32) {
-        const int i = e / B, j = e - i * B;
-        const int c = cur[(long long)(by + i) * a.W + bx + j];
-        const int y = min(max(by + i + dy, 0), a.H - 1), x = min(max(bx + j + dx, 0), a.W - 1);
-        const int d = c - (int)ref[(long long)y * a.W + x];
-        s += (uint32_t)(d * d);
+    if (bi < a.nb) {
+        const int bx = (bi % a.nbx) * B, by = (bi / a.nbx) * B;
+        const uint32_t m = a.mv[(long long)pair * a.nb + bi];
+        const int dx = (int)(int16_t)(m & 0xffff), dy = (int)(int16_t)(m >> 16);
+        const int y = by + row, x = bx;
+        uint32_t c[W4];
+        if (B == 8) {
+            const uint2 v = *reinterpret_cast<const uint2*>(cur + (long long)y * a.W + x);
+            c[0] = v.x; c[W4 - 1] = v.y;
+        } else {
+            const uint4 v = *reinterpret_cast<const uint4*>(cur + (long long)y * a.W + x);
+            c[0] = v.x; c[1] = v.y; c[2] = v.z; c[W4 - 1] = v.w;
+        }
+        const int rx = x + dx, ry = y + dy;
+        const bool inside = bx + dx >= 0 && bx + dx + B <= a.W && by + dy >= 0 && by + dy + B <= a.H;
+        uint32_t r[W4];
+        if (inside) {  // interior: aligned words, funnel-shifted (rows never cross the frame)
+            const uint8_t* rp = ref + (long long)ry * a.W + rx;
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(rp) & ~(uintptr_t)3);
+            const int sh = (int)(reinterpret_cast<uintptr_t>(rp) & 3) * 8;
+            uint32_t wv[W4 + 1];
+#pragma unroll
+            for (int k = 0; k < W4; k++) wv[k] = __ldg(w + k);
+            // the last word only when the row is unaligned (never read past the frame)
+            wv[W4] = sh ? __ldg(w + W4) : 0u;
+#pragma unroll
+            for (int k = 0; k < W4; k++) r[k] = __funnelshift_r(wv[k], wv[k + 1], sh);
+        } else {  // border: clamped bytes (reading C9)
+            const int yy = min(max(ry, 0), a.H - 1);
+#pragma unroll
+            for (int k = 0; k < W4; k++) {
+                uint32_t v = 0;
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int xx = min(max(rx + 4 * k + q, 0), a.W - 1);
+                    v |= (uint32_t)ref[(long long)yy * a.W + xx] << (8 * q);
+                }
+                r[k] = v;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < W4; k++) {
+            const uint32_t d = __vabsdiffu4(c[k], r[k]);
+            s = __dp4a(d, d, s);
+        }
     }
     s = __reduce_add_sync(FULL, s);
-    if (lane == 0) atomicAdd(&a.sse[pair], (unsigned long long)s);
+    __shared__ uint32_t ws[8];
+    if (lane == 0) ws[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) t += ws[w];
+        if (t) atomicAdd(&a.sse[pair], (unsigned long long)t);
+    }
 }
 
 // Table-IX-style quality of a motion field against the FS field (P:342 aspects 5 and 6):

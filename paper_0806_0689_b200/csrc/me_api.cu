@@ -417,8 +417,10 @@ int run_mc_sse(const uint8_t* cur0, const uint8_t* ref0, long long stride, int n
     a.mv = reinterpret_cast<const uint32_t*>(mv);
     a.sse = reinterpret_cast<unsigned long long*>(sse);
     CK(cudaMemsetAsync(sse, 0, sizeof(uint64_t) * (size_t)npairs, s));
-    dim3 grid((a.nb + 7) / 8, npairs);
-    me::mc_sse_kernel<<<grid, 256, 0, s>>>(a);
+    const int per_cta = 8 * (32 / block);  // 8 warps, 32 / B blocks per warp
+    dim3 grid((a.nb + per_cta - 1) / per_cta, npairs);
+    if (block == 16) me::mc_sse_kernel<16><<<grid, 256, 0, s>>>(a);
+    else me::mc_sse_kernel<8><<<grid, 256, 0, s>>>(a);
     g_launches++;
     CK(cudaGetLastError());
     return ME_OK;

@@ -94,3 +94,40 @@ def compare_bmas(frames: torch.Tensor, B: int, p: int, algs=TABLE9_ALGS, fs: boo
         for alg, row in out.items():
             row["nsp_speedup_of_dcds"] = row["nsp"] / base - 1.0
     return out
+
+
+def pair_series(frames: torch.Tensor, B: int, p: int, algs=("dcds", "dcds_s", "fs"), first_frame: int = 1):
+    """Per-pair (per-frame) series of the paper's frame-wise comparison (Figs. 8-9:
+    PSNR and NSP frame by frame; plus MAD, MSE, distance and probability against FS): a list of
+    {"frame", "algorithm", "mad", "mse", "nsp", "psnr_db", "dist", "prob"} in frame order, the
+    frame number of pair t being first_frame + t (the current frame of the pair)."""
+    n, _, H, W = frames.shape
+    nb = (W // B) * (H // B)
+    f = me.alloc_outputs(n, nb, frames.device)
+    me.me_fullsearch_batch(frames, B, p, *f)
+    per = {}
+    for alg in algs:
+        if alg == "fs":
+            d = f
+        else:
+            d = me.alloc_outputs(n, nb, frames.device)
+            me.me_bma_batch(alg, frames, B, p, *d)
+        q = me.me_quality_batch(d[0], f[0])
+        torch.cuda.synchronize()
+        per[alg] = pair_rows(d[3], q, W, H, B)
+    out = []
+    for t in range(n):
+        for alg in algs:
+            out.append({"frame": first_frame + t, "algorithm": alg, **per[alg][t]})
+    return out
+
+
+def series_csv(rows) -> str:
+    """SPEC's per-frame CSV layout: frame, algorithm, mad, mse, nsp, psnr_db, dist,
+    prob with 6 decimals and an `inf` sentinel for an exact match."""
+    lines = ["frame,algorithm,mad,mse,nsp,psnr_db,dist,prob"]
+    for r in rows:
+        ps = "inf" if math.isinf(r["psnr_db"]) else f"{r['psnr_db']:.6f}"
+        lines.append(f"{r['frame']},{r['algorithm']},{r['mad']:.6f},{r['mse']:.6f},{r['nsp']:.6f},{ps},"
+                     f"{r['dist']:.6f},{r['prob']:.6f}")
+    return "\n".join(lines) + "\n"

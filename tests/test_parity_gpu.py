@@ -491,3 +491,30 @@ def test_mvp_statistics_of_fs_fields():
     P = mvstats.normalise(h)
     hs, vs = mvstats.axis_shares(mvstats.quarter(P))
     assert 0 < vs < hs < 1  # the synthetic mix is horizontally biased (2:1, BASELINE configs)
+
+
+def test_per_frame_series_matches_oracle():
+    """report.pair_series (the per-frame PSNR / NSP series of P:387-413) on c1: every DCDS row
+    equals the oracle's per-pair MAD, MSE, NSP and PSNR; distance / probability against the
+    oracle's FS field; FS against itself is (0, 1)."""
+    from paper_0806_0689_b200 import report
+    cfg = synth.CONFIGS["c1"]
+    fr = synth.make_sequence(cfg, device=DEV, pairs=range(1, 7))
+    rows = report.pair_series(fr, cfg.B, cfg.p, ("dcds", "fs"), first_frame=1)
+    host = fr.cpu().numpy()
+    assert [r["frame"] for r in rows if r["algorithm"] == "dcds"] == list(range(1, 7))
+    for t in range(6):
+        omv, osad, opts = oracle.dcds(host[t, 0], host[t, 1], cfg.B, cfg.p)
+        fmv, _, _ = oracle.fullsearch(host[t, 0], host[t, 1], cfg.B, cfg.p)
+        ps, sse = oracle.mc_psnr(host[t, 0], host[t, 1], cfg.B, omv)
+        d = next(r for r in rows if r["frame"] == t + 1 and r["algorithm"] == "dcds")
+        assert d["nsp"] == opts.astype(np.int64).sum() / cfg.nb
+        assert d["mad"] == osad.astype(np.int64).sum() / (cfg.nb * cfg.B * cfg.B)
+        assert d["mse"] == sse / (cfg.W * cfg.H) and abs(d["psnr_db"] - ps) <= 1e-9
+        hits = (omv == fmv).all(1)
+        dist = np.sqrt(((omv.astype(np.float64) - fmv) ** 2).sum(1))
+        assert d["prob"] == hits.sum() / cfg.nb and abs(d["dist"] - dist.sum() / cfg.nb) < 1e-12
+        f = next(r for r in rows if r["frame"] == t + 1 and r["algorithm"] == "fs")
+        assert f["prob"] == 1.0 and f["dist"] == 0.0 and f["nsp"] == (2 * cfg.p + 1) ** 2
+    csv = report.series_csv(rows)
+    assert csv.splitlines()[0] == "frame,algorithm,mad,mse,nsp,psnr_db,dist,prob" and len(csv.splitlines()) == 13
