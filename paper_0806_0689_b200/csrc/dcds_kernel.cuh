@@ -78,6 +78,14 @@ __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
+// Shared-memory word load executed only when `p` (predicated: a lane with p false makes no
+// shared-memory access and keeps `v`) -- slot loads without a branch per slot.
+__device__ __forceinline__ uint32_t lds_if(uint32_t saddr, bool p, uint32_t v) {
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u32 %0, [%1];\n}"
+        : "+r"(v) : "r"(saddr), "r"((int)p));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t ssd4(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d = __vabsdiffu4(a, b);
     return __dp4a(d, d, c);
@@ -238,7 +246,13 @@ struct GroupState {
     // 8x8 blocks: a slot with no new point gets the sum SENT (> any SAD, 255*64 = 16320) so
     // the argmin needs no mask; 16x16 SADs (<= 65280) leave no room in the 16-bit fields.
     static constexpr bool SENTINEL = (B == 8);
+#ifdef ME_V14
     static constexpr uint32_t SENT_LANE = 16384u / G;
+#else
+    // 16376 = 8 * 2047: the group sum of a slot with no new point; as a packed key
+    // 16376 * 4 + slot >= 65504 > any SAD key (16320 * 4 + 3) and < 2^16
+    static constexpr uint32_t SENT_LANE = 16376u / G;
+#endif
     // TRACE builds only (me_dcds_trace_batch): one record per scoring pass of the block,
     // bits 0-7 pass (0 = Step 1), 8-11 pattern row (15 = HCSP), 12-19 slots scored,
     // 20-27 / 28-35 pattern centre dx / dy (int8), 36-51 incumbent SAD after the pass
@@ -425,6 +439,7 @@ struct GroupState {
         // ---- SADs of the 4 slots over this lane's rows, packed and reduced over the group
         const int o = cpos + jrow;
         uint32_t sadk[4];
+#ifndef ME_PRED_SLOTS
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             uint32_t acc = SENTINEL ? SENT_LANE : 0u;
@@ -442,6 +457,32 @@ struct GroupState {
             }
             sadk[k] = acc;
         }
+#else
+        // (experiment, measured slower on B200: c3 1.578 vs 1.465 ms, c4 18.7 vs 16.9 ms)
+        // no branch per slot: every slot's row words are loaded under the slot's predicate (a
+        // lane whose slot is not new makes no shared-memory access), its SAD is computed
+        // regardless and replaced by the sentinel / masked out of the argmin below
+        const uint32_t sbase = smem_u32(s);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const bool nk = (m4 >> k) & 1;
+            const int db = (k & 2) ? db1 : db0;
+            const int ok = (k & 1) ? o + db : o - db;
+            ME_CHECK(!nk || (ok >= 0 && ok + (R - 1) * rstride + 4 * W4 + 4 <= dbg_region));
+            const uint32_t a0 = sbase + (uint32_t)(ok & ~3);
+            const uint32_t sh = (uint32_t)ok << 3;  // funnel shifts use the low 5 bits
+            uint32_t acc = 0;
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                uint32_t wv[W4 + 1];
+#pragma unroll
+                for (int w = 0; w <= W4; w++) wv[w] = lds_if(a0 + r * rstride + 4 * w, nk, 0u);
+#pragma unroll
+                for (int w = 0; w < W4; w++) acc = vsad4(cw[r][w], __funnelshift_r(wv[w], wv[w + 1], sh), acc);
+            }
+            sadk[k] = SENTINEL ? (nk ? acc : SENT_LANE) : acc;
+        }
+#endif
         uint32_t v01 = sadk[0] | (sadk[1] << 16), v23 = sadk[2] | (sadk[3] << 16);
 #pragma unroll
         for (int q = 1; q < G; q <<= 1) {
@@ -452,8 +493,15 @@ struct GroupState {
         // ---- argmin over the new points of this pass, (SAD, slot) keys (reading C6/C7)
         uint32_t key;
         if constexpr (SENTINEL) {
+#ifdef ME_V14
             key = min(min(((v01 & 0xffffu) << 2) | 0u, ((v01 >> 16) << 2) | 1u),
                       min(((v23 & 0xffffu) << 2) | 2u, ((v23 >> 16) << 2) | 3u));
+#else
+            // packed 16-bit keys SAD * 4 + slot (SAD <= 16376: no carry between the halves),
+            // min of the two halves of each, then of the two
+            const uint32_t m = __vminu2((v01 << 2) + 0x00010000u, (v23 << 2) + 0x00030002u);
+            key = min(m & 0xffffu, m >> 16);
+#endif
         } else {
             key = 0xffffffffu;
             const uint32_t sv[4] = {v01 & 0xffffu, v01 >> 16, v23 & 0xffffu, v23 >> 16};

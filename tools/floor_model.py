@@ -278,7 +278,127 @@ def model_d3(d, pairs, tbx=16, tby=4, wx=16, wy=1, pitch=None, pitchT=None, s4_r
     return {k: v / nblk for k, v in tot.items()} | {"pitch": pitch, "pitchT": pitchT}
 
 
-def model_d0(d, pairs, pitch=192):
+def model_g1(d, pairs, tbx=16, tby=4, wx=16, wy=2, pitch=192):
+    """one thread per block, per-slot loads (8 rows x 3 words of each new slot), region as the
+    round-1 kernel (no transposed copy); a warp issues a slot's loads if any thread needs it"""
+    W, H, B, p = int(d["W"]), int(d["H"]), int(d["B"]), int(d["p"])
+    nbx, nby = W // B, H // B
+    wid, lane, tx0, ty0 = warp_layout(nbx, nby, tbx, tby, wx, wy)
+    nwarp = wid.max() + 1
+    nl = wx * wy
+    bxs = (np.arange(nbx * nby) % nbx) * B
+    bys = (np.arange(nbx * nby) // nbx) * B
+    xs = (tx0 * B - p) & ~15
+    ys = ty0 * B - p
+    ox, oy = bxs - xs, bys - ys
+    SL = {2: [(-2, 0), (2, 0), (0, -1), (0, 1)], 3: [(-1, 0), (1, 0), (0, -2), (0, 2)],
+          4: [(-1, 0), (1, 0), (0, 0), (0, 0)], 5: [(0, -1), (0, 1), (0, 0), (0, 0)]}
+    sdx = np.zeros((16, 4), np.int64)
+    sdy = np.zeros((16, 4), np.int64)
+    for k, v in SL.items():
+        sdx[k] = [o[0] for o in v]
+        sdy[k] = [o[1] for o in v]
+    tot = dict(lds=0, wf=0, lane_loads=0, warp_passes=0)
+    for pr in pairs:
+        pid, mask, cx, cy, act = decode_all(d["trace"][pr], d["tlen"][pr])
+        tab = -np.ones((nwarp, nl), np.int64)
+        tab[wid, lane] = np.arange(nbx * nby)
+        okb = tab >= 0
+        tabc = np.where(okb, tab, 0)
+        tot["warp_passes"] += int(np.where(okb, d["tlen"][pr][tabc], 0).max(axis=1).sum())
+        for i in range(1, pid.shape[1]):
+            a = act[tabc, i] & okb
+            if not a.any():
+                break
+            wsel = a.any(axis=1)
+            blk = tabc[wsel]
+            A = a[wsel]
+            pi = pid[blk, i]
+            for k in range(4):
+                need = A & (((mask[blk, i] >> k) & 1) == 1)
+                ws = need.any(axis=1)
+                if not ws.any():
+                    continue
+                o = (oy[blk] + cy[blk, i] + sdy[pi, k]) * pitch + ox[blk] + cx[blk, i] + sdx[pi, k]
+                for r in range(8):
+                    for w in range(3):
+                        addr = (o + r * pitch) // 4 + w
+                        wf = wavefronts(addr[ws], need[ws])
+                        tot["wf"] += int(wf.sum())
+                        tot["lds"] += int(ws.sum())
+                        tot["lane_loads"] += int(need[ws].sum())
+    nblk = len(pairs) * nbx * nby
+    return {k: v / nblk for k, v in tot.items()}
+
+
+def model_d0_refill(d, pairs, pitch=192, nwarps=4, tbx=16, tby=4, refill_at=1):
+    """D0's loads (G = 2, 4 slots x 8 rows x 3 words, 16 groups per warp) when groups are
+    refilled: a CTA's nwarps warps share the tile's block counter, a group that finished takes
+    the next block of the tile (raster order) at the next warp-pass (refill_at: only when at
+    least that many groups of the warp are idle).  Returns the slot-load counts and the
+    warp-passes per block (the issue / ALU side)."""
+    W, H, B, p = int(d["W"]), int(d["H"]), int(d["B"]), int(d["p"])
+    nbx, nby = W // B, H // B
+    SL = {2: [(-2, 0), (2, 0), (0, -1), (0, 1)], 3: [(-1, 0), (1, 0), (0, -2), (0, 2)],
+          4: [(-1, 0), (1, 0), (0, 0), (0, 0)], 5: [(0, -1), (0, 1), (0, 0), (0, 0)]}
+    tot = dict(lds=0, wf=0, lane_loads=0, warp_passes=0, refill_events=0)
+    for pr in pairs:
+        pid, mask, cx, cy, act = decode_all(d["trace"][pr], d["tlen"][pr])
+        tl = d["tlen"][pr]
+        for ty in range(nby // tby):
+            for tx in range(nbx // tbx):
+                x0, y0 = tx * tbx * B, ty * tby * B
+                xs, ys = (x0 - p) & ~15, y0 - p
+                queue = [(y0 // B + a) * nbx + x0 // B + b for a in range(tby) for b in range(tbx)]
+                qi = 0
+                cur = [[None] * 16 for _ in range(nwarps)]   # (block, pass index)
+                while True:
+                    alive = False
+                    for w in range(nwarps):
+                        idle = [g for g in range(16) if cur[w][g] is None]
+                        if idle and qi < len(queue) and len(idle) >= min(refill_at, len(queue) - qi):
+                            tot["refill_events"] += 1
+                            for g in idle:
+                                if qi < len(queue):
+                                    cur[w][g] = [queue[qi], 0]
+                                    qi += 1
+                        groups = [(g, c) for g, c in enumerate(cur[w]) if c is not None]
+                        if not groups:
+                            continue
+                        alive = True
+                        tot["warp_passes"] += 1
+                        for k in range(4):
+                            addrs, n = [], 0
+                            for g, (blk, i) in groups:
+                                if i == 0:
+                                    continue  # step 1: aligned loads, not a slot load
+                                if not (mask[blk, i] >> k) & 1:
+                                    continue
+                                dx, dy = SL[int(pid[blk, i])][k]
+                                ox = (blk % nbx) * B - xs
+                                oy = (blk // nbx) * B - ys
+                                o = (oy + int(cy[blk, i]) + dy) * pitch + ox + int(cx[blk, i]) + dx
+                                addrs.append(o)
+                            if not addrs:
+                                continue
+                            o = np.array(addrs)
+                            for r in range(4):
+                                for wd in range(3):
+                                    words = np.concatenate([(o + 2 * r * pitch) // 4 + wd, (o + (2 * r + 1) * pitch) // 4 + wd])
+                                    tot["wf"] += int(wavefronts(words[None, :], np.ones((1, words.size), bool))[0])
+                                    tot["lds"] += 1
+                                    tot["lane_loads"] += words.size
+                        for g, c in groups:
+                            c[1] += 1
+                            if c[1] >= tl[c[0]]:
+                                cur[w][g] = None
+                    if not alive:
+                        break
+    nblk = len(pairs) * (nbx // tbx * tbx) * (nby // tby * tby)
+    return {k: v / nblk for k, v in tot.items()}
+
+
+def model_d0(d, pairs, pitch=192, swap=None):
     """the round-1 kernel: G=2, 16 blocks per warp (16x4 tiles), 4 slots x 8 rows x 3 words"""
     W, H, B, p = int(d["W"]), int(d["H"]), int(d["B"]), int(d["p"])
     nbx, nby = W // B, H // B
@@ -319,10 +439,15 @@ def model_d0(d, pairs, pitch=192):
                     continue
                 ws = need.any(axis=1)
                 o = (oy[blk] + cy[blk, i] + sdy[pi, k]) * pitch + ox[blk] + cx[blk, i] + sdx[pi, k]
+                gpar = (np.arange(16)[None, :] % 2) if swap == "g" else (
+                    (np.arange(16)[None, :] // 2) % 2 if swap == "g2" else np.zeros((1, 16), np.int64))
                 for r in range(4):
                     for w in range(3):
-                        # two lanes per group: rows j + 2r, j = 0, 1
-                        addr = np.concatenate([(o + (2 * r) * pitch) // 4 + w, (o + (2 * r + 1) * pitch) // 4 + w], axis=1)
+                        # two lanes per group: rows j + 2r, j = 0, 1 (swap: odd groups' lanes
+                        # exchange rows, so lane 0 reads row 2r + 1)
+                        r0 = 2 * r + gpar
+                        r1 = 2 * r + 1 - gpar
+                        addr = np.concatenate([(o + r0 * pitch) // 4 + w, (o + r1 * pitch) // 4 + w], axis=1)
                         val = np.concatenate([need, need], axis=1)
                         wf = wavefronts(addr[ws], val[ws])
                         tot["wf"] += int(wf.sum())
