@@ -70,6 +70,7 @@ struct SearchArgs {
     uint64_t* trace;            // TRACE builds: [npairs][nb][tcap] pass records
     uint16_t* tlen;             // TRACE builds: [npairs][nb] passes of each block
     int tcap;
+    int pf;                     // L2 prefetch distance in CTAs (0: none)
 };
 
 __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
@@ -120,6 +121,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
+}
+
+// L2 prefetch of a 3-D tensor-map box (no shared-memory destination, no completion).
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z)
+                 : "memory");
 }
 
 // Edge replication (reading C9) of a TMA-staged region whose box reached outside the frame
@@ -600,6 +608,19 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
         tma_load_3d(sref, &tm_ref, xs, ys, pair, bar);
         tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
         *ctr = 0;
+        if (a.pf) {
+            // warm L2 with the tile of the CTA about one resident wave later (CTAs are
+            // scheduled in linear order), so its staging waits on L2 instead of HBM
+            const long long lin = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z) + a.pf;
+            const long long per = (long long)gridDim.x * gridDim.y;
+            if (lin < per * gridDim.z) {
+                const int fz = (int)(lin / per), fr = (int)(lin - (long long)fz * per);
+                const int fy = fr / gridDim.x, fx = fr - fy * gridDim.x;
+                const int fx0 = fx * TW, fy0 = fy * TH;
+                tma_prefetch_3d(&tm_ref, (fx0 - a.p) & ~15, fy0 - a.p, fz);
+                tma_prefetch_3d(&tm_cur, fx0, fy0, fz);
+            }
+        }
     }
     const int bw = bm_row(p);
     // bitmap template: border bits set (rows < 2 or >= 2p+3, columns < 2 of the row length)
