@@ -566,7 +566,7 @@ struct GroupState {
 // produced in one dense phase after the last search ends.  Otherwise blocks are handed out
 // from a tile counter as groups finish.
 template <int B, int G, int NWARP, int VARIANT, bool TRACE = false, bool ONE = false, int PITCH = 0>
-__global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 9 : 1)
+__global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
     dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
                 const SearchArgs a) {
     static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "lane-group size");

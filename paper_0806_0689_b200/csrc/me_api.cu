@@ -29,6 +29,7 @@ unsigned long long* g_scratch = nullptr;  // device u64 scratch (me_mc_psnr)
 char g_err[512] = "";
 long long g_launches = 0;
 int g_smem_optin = 0;
+int g_sms = 148;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;  // driver entry point (no -lcuda)
 
 // grow-only staging buffers of me_dcds_batch_host (two sets for double buffering)
@@ -160,7 +161,7 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     a.cur_off = (pitch * a.rh + 127) & ~127;
     L.TW = TW; L.TH = TH;
     // the ONE kernels (one block per lane group) exist for the default geometry
-    L.one = tbx * tby <= groups && L.G == (B == 16 ? 8 : 2) && L.NW == (B == 16 ? 8 : 4);
+    L.one = tbx * tby <= groups && L.G == (B == 16 ? 8 : 2) && (L.NW == (B == 16 ? 8 : 4) || (B == 8 && L.NW == 8));
     const int bm_bytes = (groups + 4) * a.bm_words * 4;  // interleaved, word stride groups + 4
     if (L.one) {  // bitmaps overlay the current tile (read into registers first)
         a.bm_off = a.cur_off;
@@ -182,6 +183,12 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
 template <int B, int G, int VARIANT>
 void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap& tr, cudaStream_t s) {
     constexpr int DG = B == 16 ? 8 : 2, DNW = B == 16 ? 8 : 4;  // default geometry
+    if constexpr (G == DG && B == 8) {
+        if (L.one && L.NW == 8) {  // 8x8 blocks, 16x8 tiles of 8 warps (tuning: ME_NW=8 ME_TILE=16,8)
+            me::dcds_kernel<8, 2, 8, VARIANT, false, true><<<L.grid, 256, L.smem, s>>>(tc, tr, L.a);
+            return;
+        }
+    }
     if constexpr (G == DG) {
         if (L.one) {
             // the bench geometries (B=8: 16x4 tiles, +-16; B=16: 4x8 tiles, +-32) also exist
@@ -474,6 +481,7 @@ int me_init(int device) {
         return ME_ECUDA;
     }
     g_smem_optin = (int)prop.sharedMemPerBlockOptin;
+    g_sms = prop.multiProcessorCount;
     int rc;
 #define ME_ALLOW(B, G, V) \
     if ((rc = allow_smem(me::dcds_kernel<B, G, 2, V>))) return rc;             \
@@ -486,6 +494,8 @@ int me_init(int device) {
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true, 176>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true, 176>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, false, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 8, 0, false, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<8, 2, 8, 1, false, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, false, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true>))) return rc;

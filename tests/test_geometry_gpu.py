@@ -69,6 +69,7 @@ GEOMS = [
     (8, {"ME_G": "4"}),
     (8, {"ME_G": "8", "ME_NW": "2"}),
     (8, {"ME_NW": "8", "ME_TILE": "16,4"}),
+    (8, {"ME_NW": "8", "ME_TILE": "16,8"}),  # ONE with 8 warps (tuning knob; measured slower)
     (16, {"ME_TILE": "8,8"}),            # G=8, 8 warps, 64 blocks for 32 groups: hand-out
     (16, {"ME_TILE": "4,2"}),            # ONE with idle groups
     (16, {"ME_G": "4", "ME_NW": "4"}),
