@@ -17,10 +17,14 @@
  *   - Table VIII distribution 2, Table II weighted by the NSP map;
  *   - FS against an independent numpy brute force; zero-noise translations (closed form);
  *   - PSNR closed forms.
+ *   - DCDS^S's side rule (the middle point beside the cheaper distant point) by hand
+ *     traces on the ideal surface and the exact p=7 miss set; the same file compiled with
+ *     the side reversed fails them (tests/test_oracle_pins.py, mutation test).
  * Parity unpinned vs the paper (conventions where it is silent; pinned oracle<->GPU only):
  * the order among the new points of a pattern (C7), the FS tie rule (C13) and DCDS^S's tie
- * rule (C22); h-/v-HEXBS (C25) is pinned only weakly (Table VI pattern mass, zero-motion NSP
- * 11, Table VIII distribution 2 within 0.1).
+ * side / infeasible-distant rule (C22); h-/v-HEXBS (C25) is pinned only weakly (Table VI
+ * pattern mass, zero-motion NSP 11, Table VIII both rows: the printed values are this
+ * reading's ANSP cut to one decimal).
  */
 #include "oracle.h"
 
