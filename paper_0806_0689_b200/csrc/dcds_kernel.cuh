@@ -165,7 +165,7 @@ __device__ __forceinline__ void fixup_edges(uint8_t* sref, int pitch, int rh, in
 template <int R, int W4>
 __device__ __forceinline__ void ref_rows(const uint32_t* s, int o, int rstride,
                                          uint32_t (&out)[R][W4]) {
-    const int sh = (o & 3) << 3;
+    const int sh = o << 3;  // funnel shifts use the low 5 bits: (o & 3) * 8
     const uint32_t* b = s + (o >> 2);
 #pragma unroll
     for (int r = 0; r < R; r++) {
@@ -246,6 +246,36 @@ enum : int { ST_DONE = 0, ST_S1A = 1, ST_S3 = 3, ST_S4 = 4, ST_S4PRE = 5, ST_IDL
 __host__ __device__ constexpr int bm_row(int p) { return 2 * p + 3; }
 __host__ __device__ constexpr int bm_nwords(int p) { return ((2 * p + 5) * bm_row(p) + 2 + 31) / 32; }
 
+
+// The two bitmap templates of window +-p (word t of the bordered bitmap): border bits set
+// (rows < 2 or >= 2p+3, the 2 border columns between rows), and with_hcsp the 7 HCSP points of
+// Step 1 at the window origin as well.  me_init evaluates them once for every p in
+// [1, 32] into constant memory (c_bm_tmpl); the kernels copy them instead of rebuilding them
+// per CTA.
+__host__ __device__ inline uint32_t bm_template_word(int p, int t, bool with_hcsp) {
+    const int bw = bm_row(p), lo = 32 * t;
+    auto span = [lo](int b0, int b1) -> uint32_t {  // bits [b0, b1) of [lo, lo + 32)
+        b0 = b0 > lo ? b0 : lo;
+        b1 = b1 < lo + 32 ? b1 : lo + 32;
+        return b1 > b0 ? (uint32_t)(((1ull << (b1 - b0)) - 1ull) << (b0 - lo)) : 0u;
+    };
+    uint32_t w = span(0, 2 * bw) | span((2 * p + 3) * bw, lo + 32);
+    for (int rs = (lo / bw) * bw; rs < lo + 32; rs += bw) w |= span(rs, rs + 2);
+    if (with_hcsp) {
+        const int c = (p + 2) * bw + p + 2;
+        const int hc[7] = {c, c - 1, c + 1, c - 2, c + 2, c - bw, c + bw};
+        for (int k = 0; k < 7; k++)
+            if (hc[k] >= lo && hc[k] < lo + 32) w |= 1u << (hc[k] - lo);
+    }
+    return w;
+}
+__host__ __device__ constexpr int bm_tmpl_off(int p) {  // words before p's two templates
+    int o = 0;
+    for (int q = 1; q < p; q++) o += 2 * bm_nwords(q);
+    return o;
+}
+constexpr int BM_TMPL_WORDS = bm_tmpl_off(33);
+__constant__ uint32_t c_bm_tmpl[BM_TMPL_WORDS];
 
 template <int B, int G, bool TRACE = false>
 struct GroupState {
@@ -623,24 +653,10 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
         }
     }
     const int bw = bm_row(p);
-    // bitmap template: border bits set (rows < 2 or >= 2p+3, columns < 2 of the row length)
+    // bitmap templates (border only / border + HCSP), precomputed in constant memory
     for (int t = threadIdx.x; t < a.bm_words; t += NWARP * 32) {
-        const int lo = 32 * t;
-        // bits [b0, b1) of the word's range [lo, lo + 32)
-        auto span = [lo](int b0, int b1) -> uint32_t {
-            b0 = max(b0, lo); b1 = min(b1, lo + 32);
-            return b1 > b0 ? (uint32_t)(((1ull << (b1 - b0)) - 1ull) << (b0 - lo)) : 0u;
-        };
-        uint32_t w = span(0, 2 * bw) | span((2 * p + 3) * bw, lo + 32);
-        for (int rs = (lo / bw) * bw; rs < lo + 32; rs += bw) w |= span(rs, rs + 2);
-        bm_win[t] = w;
-        // the HCSP points of Step 1, scored by every block at the window origin
-        const int c = (p + 2) * bw + p + 2;
-        const int hc[7] = {c, c - 1, c + 1, c - 2, c + 2, c - bw, c + bw};
-#pragma unroll
-        for (int k = 0; k < 7; k++)
-            if (hc[k] >= lo && hc[k] < lo + 32) w |= 1u << (hc[k] - lo);
-        bm_init[t] = w;
+        bm_win[t] = c_bm_tmpl[bm_tmpl_off(p) + t];
+        bm_init[t] = c_bm_tmpl[bm_tmpl_off(p) + a.bm_words + t];
     }
     mbar_wait(bar, 0);
     if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)

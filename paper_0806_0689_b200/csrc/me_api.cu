@@ -518,6 +518,17 @@ int me_init(int device) {
     if ((rc = allow_smem(me::fs_kernel<16>))) return rc;
     if ((rc = allow_smem(me::fs_kernel<8>))) return rc;
     if (!g_scratch) CK(cudaMalloc(&g_scratch, 64));
+    {  // visited-bitmap templates for every p (dcds_kernel.cuh, bm_template_word)
+        static uint32_t tmpl[me::BM_TMPL_WORDS];
+        for (int q = 1; q <= 32; q++) {
+            const int nw = me::bm_nwords(q), off = me::bm_tmpl_off(q);
+            for (int t = 0; t < nw; t++) {
+                tmpl[off + t] = me::bm_template_word(q, t, false);
+                tmpl[off + nw + t] = me::bm_template_word(q, t, true);
+            }
+        }
+        CK(cudaMemcpyToSymbol(me::c_bm_tmpl, tmpl, sizeof tmpl));
+    }
     if (!g_encode) {
         cudaDriverEntryPointQueryResult q;
         CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&g_encode),
