@@ -63,9 +63,10 @@ def lib() -> ctypes.CDLL:
         L.oracle_mc_psnr.argtypes = [u8p, u8p, c_int, c_int, c_int, i16p, dp, u64p]
         L.oracle_dcds_cost.argtypes = [COST_FN, ctypes.c_void_p, c_int, c_int, ip, ip, dp, ip, ip, c_int, ip]
         L.oracle_ideal_nsp_map.argtypes = [c_int, c_int, ip, ip, ip]
+        L.oracle_quality.argtypes = [i16p, i16p, c_int, ip, dp]
         for f in (L.oracle_sad, L.oracle_sse_block, L.oracle_dcds, L.oracle_fullsearch,
                   L.oracle_mc_psnr, L.oracle_dcds_cost, L.oracle_ideal_nsp_map,
-                  L.oracle_dcds_block, L.oracle_fullsearch_block):
+                  L.oracle_dcds_block, L.oracle_fullsearch_block, L.oracle_quality):
             f.restype = c_int
         _lib = L
     return _lib
@@ -208,3 +209,16 @@ def ideal_nsp_map(p, variant: int = 0):
     _check(lib().oracle_ideal_nsp_map(p, variant, _ptr(nsp, ctypes.c_int), _ptr(mx, ctypes.c_int),
                                       _ptr(my, ctypes.c_int)), "oracle_ideal_nsp_map")
     return nsp.reshape(side, side), mx.reshape(side, side), my.reshape(side, side)
+
+
+def quality(mv, mv_fs):
+    """(hits, sum of Euclidean distances) of an MV field [nb, 2] against the FS field
+    (P:342 aspects 5-6)."""
+    mv = np.ascontiguousarray(mv, dtype=np.int16)
+    mv_fs = np.ascontiguousarray(mv_fs, dtype=np.int16)
+    if mv.shape != mv_fs.shape or mv.ndim != 2 or mv.shape[1] != 2:
+        raise ValueError("mv and mv_fs must be equal-shape [nb, 2] fields")
+    h, d = ctypes.c_int(), ctypes.c_double()
+    _check(lib().oracle_quality(_ptr(mv, ctypes.c_int16), _ptr(mv_fs, ctypes.c_int16), mv.shape[0],
+                                ctypes.byref(h), ctypes.byref(d)), "oracle_quality")
+    return h.value, d.value

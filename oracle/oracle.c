@@ -480,3 +480,21 @@ int oracle_mc_psnr(const uint8_t* cur, const uint8_t* ref, int W, int H, int B,
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* Quality against FS (P:43, P:342 aspects 5-6).                      */
+/* ------------------------------------------------------------------------------------ */
+int oracle_quality(const int16_t* mv, const int16_t* mv_fs, int nb, int* hits, double* dist) {
+    if (!mv || !mv_fs || nb < 1 || !hits || !dist) return -1;
+    int h = 0;
+    double d = 0.0;
+    for (int i = 0; i < nb; i++) {
+        int ex = (int)mv[2 * i] - (int)mv_fs[2 * i];
+        int ey = (int)mv[2 * i + 1] - (int)mv_fs[2 * i + 1];
+        if (ex == 0 && ey == 0) h++;
+        d += sqrt((double)(ex * ex + ey * ey));
+    }
+    *hits = h;
+    *dist = d;
+    return 0;
+}

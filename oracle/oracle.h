@@ -66,6 +66,12 @@ int oracle_fullsearch_block(const uint8_t* cur, const uint8_t* ref, int W, int H
 int oracle_mc_psnr(const uint8_t* cur, const uint8_t* ref, int W, int H, int B,
                    const int16_t* mv, double* psnr_out, uint64_t* sse_out);
 
+/* Quality of a motion field against the full-search field (P:43 / P:342 aspects 5 and 6:
+ * "the distance from the true motion vectors (obtained by FS)" and "the probability of
+ * finding the true MVs"): over nb blocks, *hits = number of blocks whose MV equals the FS MV
+ * and *dist = sum of the Euclidean distances |mv - mv_fs| (double, blocks in order). */
+int oracle_quality(const int16_t* mv, const int16_t* mv_fs, int nb, int* hits, double* dist);
+
 /* DCDS (or, by variant, a comparison BMA) on an injected cost function (the ideal
  * unimodal surface).  cost(dx,dy,ctx)
  * is called once per distinct feasible candidate.  trace (may be NULL) receives up to

@@ -460,3 +460,21 @@ def test_dcds_s_pins_reject_reversed_side(tmp_path):
     nsp, mx, my = mut_map(7, 1)
     ty, tx = np.mgrid[-7:8, -7:8]
     assert int(((mx != tx) | (my != ty)).sum()) == 62
+
+
+def test_quality_against_fs_examples():
+    """Quality vs FS (P:43, P:342 aspects 5-6): a field against itself -> every
+    block a hit, distance 0; one of two blocks off by (1,0) -> 1 hit, distance 1 (prob 0.5,
+    mean distance 0.5); every block off by (3,4) -> no hit, distance 5 each (Pythagorean);
+    and per block the distance is 0 exactly on the hits (checked on random fields)."""
+    z = np.zeros((2, 2), np.int16)
+    assert oracle.quality(z, z) == (2, 0.0)
+    assert oracle.quality(np.array([[0, 0], [1, 0]]), z) == (1, 1.0)
+    assert oracle.quality(np.array([[3, 4], [-3, -4]]), z) == (0, 10.0)
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        a = rng.integers(-2, 3, (50, 2)).astype(np.int16)
+        b = rng.integers(-2, 3, (50, 2)).astype(np.int16)
+        h, d = oracle.quality(a, b)
+        per = np.hypot(*(a.astype(float) - b).T)
+        assert h == int((per == 0).sum()) and abs(d - per.sum()) < 1e-12
