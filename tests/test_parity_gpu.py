@@ -510,9 +510,8 @@ def test_per_frame_series_matches_oracle():
         assert d["nsp"] == opts.astype(np.int64).sum() / cfg.nb
         assert d["mad"] == osad.astype(np.int64).sum() / (cfg.nb * cfg.B * cfg.B)
         assert d["mse"] == sse / (cfg.W * cfg.H) and abs(d["psnr_db"] - ps) <= 1e-9
-        hits = (omv == fmv).all(1)
-        dist = np.sqrt(((omv.astype(np.float64) - fmv) ** 2).sum(1))
-        assert d["prob"] == hits.sum() / cfg.nb and abs(d["dist"] - dist.sum() / cfg.nb) < 1e-12
+        hits, dist = oracle.quality(omv, fmv)
+        assert d["prob"] == hits / cfg.nb and abs(d["dist"] - dist / cfg.nb) < 1e-12
         f = next(r for r in rows if r["frame"] == t + 1 and r["algorithm"] == "fs")
         assert f["prob"] == 1.0 and f["dist"] == 0.0 and f["nsp"] == (2 * cfg.p + 1) ** 2
     csv = report.series_csv(rows)
