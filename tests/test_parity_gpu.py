@@ -257,6 +257,34 @@ def test_host_buffer_variant_matches_device():
     np.testing.assert_array_equal(hst.numpy().astype(np.uint64), st)
 
 
+def test_host_buffer_variant_chunks_and_padded_stride():
+    """me_dcds_batch_host over several staging chunks (128 MiB of frames per chunk: 32 c3 pairs)
+    with a host pair stride larger than 2*W*H (padding between pairs): equal to the device
+    search of the same pairs."""
+    import ctypes
+    cfg = synth.CONFIGS["c3"]
+    n = 35
+    fr = synth.make_sequence(cfg, device=DEV, pairs=range(1, n + 1))
+    mv, sad, pts, st = gpu_search(fr, cfg.B, cfg.p)
+    fsz = cfg.W * cfg.H
+    stride = 2 * fsz + 4096 + 7  # padded, odd: the ABI copies each frame on its own
+    host = torch.zeros(n * stride + 64, dtype=torch.uint8).pin_memory()
+    hf = fr.cpu().reshape(n, 2 * fsz)
+    for t in range(n):
+        host[t * stride: t * stride + fsz] = hf[t, :fsz]
+        host[t * stride + fsz + 5: t * stride + 2 * fsz + 5] = hf[t, fsz:]
+    hmv, hsad, hpts, hst = [x.pin_memory() for x in me.alloc_outputs(n, cfg.nb, "cpu")]
+    L = me.load()
+    base = host.data_ptr()
+    rc = L.me_dcds_batch_host(base, base + fsz + 5, stride, n, cfg.W, cfg.H, cfg.B, cfg.p,
+                              hmv.data_ptr(), hsad.data_ptr(), hpts.data_ptr(), hst.data_ptr())
+    assert rc == 0, L.me_strerror(rc)
+    np.testing.assert_array_equal(hmv.numpy(), mv)
+    np.testing.assert_array_equal(hsad.numpy().astype(np.uint32), sad)
+    np.testing.assert_array_equal(hpts.numpy().astype(np.uint16), pts)
+    np.testing.assert_array_equal(hst.numpy().astype(np.uint64), st)
+
+
 def test_host_buffer_variant_unrelated_single_pair():
     """me_dcds_batch_host with npairs == 1 and cur / ref in two unrelated host buffers (the
     ABI copies each frame on its own, never the span between them), odd pointer
