@@ -398,12 +398,11 @@ def model_d0_refill(d, pairs, pitch=192, nwarps=4, tbx=16, tby=4, refill_at=1):
     return {k: v / nblk for k, v in tot.items()}
 
 
-def model_d0(d, pairs, pitch=192, swap=None):
+def model_d0(d, pairs, pitch=192, swap=None, tbx=16, tby=4, wx=16, wy=1):
     """the round-1 kernel: G=2, 16 blocks per warp (16x4 tiles), 4 slots x 8 rows x 3 words"""
     W, H, B, p = int(d["W"]), int(d["H"]), int(d["B"]), int(d["p"])
     nbx, nby = W // B, H // B
-    tbx, tby = 16, 4
-    wid, lane, tx0, ty0 = warp_layout(nbx, nby, tbx, tby, 16, 1)
+    wid, lane, tx0, ty0 = warp_layout(nbx, nby, tbx, tby, wx, wy)
     nwarp = wid.max() + 1
     bxs = (np.arange(nbx * nby) % nbx) * B
     bys = (np.arange(nbx * nby) // nbx) * B
