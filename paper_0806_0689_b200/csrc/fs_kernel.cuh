@@ -299,6 +299,90 @@ __global__ void __launch_bounds__(256) mc_sse_kernel(const McArgs a) {
     }
 }
 
+// Standalone MC-SSE with TMA staging (me_mc_sse_batch / me_mc_psnr on frames at least one
+// tile large): the DCDS kernels' tile geometry (SearchArgs from plan_dcds with a fixed halo
+// hp: 16 for 8x8, 32 for 16x16 blocks) -- the tile's reference region and current tile are
+// staged by TMA (each frame byte read from HBM once; the halo re-reads hit L2) and edge-fixed
+// (reading C9).  One lane per block row (B lanes per block): the current row from the staged
+// tile, the reference row at the block's MV from the region (B/4 + 1 words, funnel-shifted),
+// squared differences by VABSDIFF4 + IDP.4A.  A block whose displaced block leaves the staged
+// region (|mv| > hp) reads the clamped reference from global memory instead (exact, rare).
+template <int B>
+__global__ void __launch_bounds__(256)
+    mc_sse_tma_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
+                      const SearchArgs a, const uint32_t* __restrict__ mvf) {
+    constexpr int W4 = B / 4;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int pair = blockIdx.z, tx = blockIdx.x, ty = blockIdx.y;
+    const int TW = a.tbx * B, TH = a.tby * B;
+    const int x0 = tx * TW, y0 = ty * TH;
+    const int xs = (x0 - a.p) & ~15, ys = y0 - a.p;
+    const int pitch = a.pitch;
+    uint8_t* sref = smem;
+    uint8_t* scur = smem + a.cur_off;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((a.cur_off + TW * TH + 7) & ~7));
+    __shared__ unsigned long long ssum[8];
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(bar, (uint32_t)(pitch * a.rh + TW * TH));
+        tma_load_3d(sref, &tm_ref, xs, ys, pair, bar);
+        tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
+    }
+    mbar_wait(bar, 0);
+    if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
+        fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
+    __syncthreads();
+    const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, a.nby - ty * a.tby);
+    const int nbt = tbx_e * tby_e;
+    const uint8_t* gref = a.ref0 + (long long)pair * a.stride;
+    uint32_t s = 0;
+    // (block, row) items: 256 threads = 256 / B blocks per round
+    for (int e = threadIdx.x; e < nbt * B; e += blockDim.x) {
+        const int lb = e / B, r = e - lb * B;
+        const int lby = lb / tbx_e, lbx = lb - lby * tbx_e;
+        const int bxg = x0 + lbx * B, byg = y0 + lby * B;
+        const uint32_t m = mvf[(long long)pair * a.nb + (byg / B) * a.nbx + bxg / B];
+        const int dx = (int)(int16_t)(m & 0xffff), dy = (int)(int16_t)(m >> 16);
+        const uint32_t* crow = reinterpret_cast<const uint32_t*>(scur + (lby * B + r) * TW + lbx * B);
+        uint32_t rw[W4];
+        if (dx >= -a.p && dx <= a.p && dy >= -a.p && dy <= a.p) {
+            const int o = (byg + r + dy - ys) * pitch + (bxg + dx - xs);  // inside the staged region
+            const uint32_t* b = reinterpret_cast<const uint32_t*>(sref) + (o >> 2);
+            uint32_t wv[W4 + 1];
+#pragma unroll
+            for (int w = 0; w <= W4; w++) wv[w] = b[w];
+#pragma unroll
+            for (int w = 0; w < W4; w++) rw[w] = __funnelshift_r(wv[w], wv[w + 1], o << 3);
+        } else {  // beyond the staged halo: clamped global reads (reading C9)
+            const int yy = min(max(byg + r + dy, 0), a.H - 1);
+#pragma unroll
+            for (int w = 0; w < W4; w++) {
+                uint32_t v = 0;
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    v |= (uint32_t)gref[(long long)yy * a.W + min(max(bxg + dx + 4 * w + q, 0), a.W - 1)] << (8 * q);
+                rw[w] = v;
+            }
+        }
+#pragma unroll
+        for (int w = 0; w < W4; w++) {
+            const uint32_t d = __vabsdiffu4(crow[w], rw[w]);
+            s = __dp4a(d, d, s);
+        }
+    }
+    // a lane's sum <= a few rows x 65025 x B: 32 bits; warp and CTA sums in 64
+    const unsigned long long sw = __reduce_add_sync(FULL, s);  // <= 32 x 2 x 65025 x 16 < 2^32
+    if (lane == 0) ssum[warp] = sw;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += ssum[w];
+        if (t) atomicAdd(&a.stats[pair], t);
+    }
+}
+
 // Table-IX-style quality of a motion field against the FS field (P:342 aspects 5 and 6):
 // per pair, the number of blocks whose MV equals the FS MV and the sum of the Euclidean
 // distances |mv - mv_fs| (double).  One CTA per pair; each thread sums a fixed strided subset

@@ -421,6 +421,33 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
 
 int run_mc_sse(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npairs, int W,
                int H, int block, const int16_t* mv, uint64_t* sse, cudaStream_t s) {
+    // frames of at least one DCDS tile: the TMA-staged kernel (the DCDS tile geometry with a
+    // fixed halo; larger MVs fall back to clamped global reads inside it); otherwise the
+    // warp-per-block kernel
+    if (!getenv("ME_MC_LEGACY")) {
+        const int hp = block == 16 ? 32 : 16;
+        DcdsLaunch L = plan_dcds(W, H, block, hp, npairs);
+        if (L.TW == (block == 16 ? 4 : 16) * block && L.TH == (block == 16 ? 8 : 4) * block) {
+            L.a.cur0 = cur0; L.a.ref0 = ref0; L.a.stride = stride;
+            L.a.stats = reinterpret_cast<unsigned long long*>(sse);
+            const size_t smem = (size_t)((L.a.cur_off + L.TW * L.TH + 7) & ~7) + 16;
+            CUtensorMap tc, tr;
+            int rc = make_tmap(&tc, cur0, W, H, npairs, stride, L.TW, L.TH);
+            if (rc) return rc;
+            rc = make_tmap(&tr, ref0, W, H, npairs, stride, L.a.pitch, L.a.rh);
+            if (rc) return rc;
+            CK(cudaMemsetAsync(sse, 0, sizeof(uint64_t) * (size_t)npairs, s));
+            const uint32_t* mvf = reinterpret_cast<const uint32_t*>(mv);
+            // measured (tools/gpu_mc.sh): 128 threads for 8x8 blocks (c3 0.318 ms vs 0.361 at 256), 256 for
+            // 16x16 (c4 4.99 ms vs 5.74 at 128)
+            const int nt = getenv("ME_MC_THREADS") ? atoi(getenv("ME_MC_THREADS")) : (block == 16 ? 256 : 128);
+            if (block == 16) me::mc_sse_tma_kernel<16><<<L.grid, nt, smem, s>>>(tc, tr, L.a, mvf);
+            else me::mc_sse_tma_kernel<8><<<L.grid, nt, smem, s>>>(tc, tr, L.a, mvf);
+            g_launches++;
+            CK(cudaGetLastError());
+            return ME_OK;
+        }
+    }
     me::McArgs a;
     a.cur0 = cur0; a.ref0 = ref0; a.stride = stride;
     a.W = W; a.H = H; a.B = block;
@@ -515,6 +542,8 @@ int me_init(int device) {
     ME_ALLOW_BMA(8, 2, 4)
     ME_ALLOW_BMA(16, 8, 8)
 #undef ME_ALLOW_BMA
+    if ((rc = allow_smem(me::mc_sse_tma_kernel<16>))) return rc;
+    if ((rc = allow_smem(me::mc_sse_tma_kernel<8>))) return rc;
     if ((rc = allow_smem(me::fs_kernel<16>))) return rc;
     if ((rc = allow_smem(me::fs_kernel<8>))) return rc;
     if (!g_scratch) CK(cudaMalloc(&g_scratch, 64));
