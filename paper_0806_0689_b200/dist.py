@@ -3,9 +3,10 @@
 Frame pairs are independent units (every block's search depends only on its own pair),
 so ranks shard pairs with no data-path exchange.  The only collective gathers the per-pair
 outputs -- the MV field (mv, SAD, points per block) and the per-pair statistics
-(sum points, sum SAD, SSE) -- with NCCL (torch.distributed) over NVLink.  This module holds
-the host logic (sharding, padded all_gather, reassembly) so it can be tested with the gloo
-backend on CPU; it contains none of the method's arithmetic.
+(sum points, sum SAD, SSE) -- with NCCL (torch.distributed) over NVLink, to rank 0 or to every
+rank.  This module holds the host logic (sharding, padded gathers, reassembly, the
+double-buffered step of bench.py) so it can be tested with the gloo backend on CPU; it contains
+none of the method's arithmetic.
 """
 from __future__ import annotations
 
