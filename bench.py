@@ -343,7 +343,8 @@ def timed_run(args, cfg, me, mdist, dist, ws, rank, dev, stream, scaling, sample
                 for k in range(args.steps):
                     search(*step.local_views(0))
             me.me_set_stream(stream)
-            launches0 = me.me_launch_count() - args.steps  # the captured launches
+            # (launches0 was read before the capture: the delta is the captured launches, which
+            # the timed replay runs once)
             graph.replay()  # warm the graph
             torch.cuda.synchronize()
             clk.mark_start()
