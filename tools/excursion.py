@@ -1,12 +1,14 @@
 """How far do the DCDS searches of a config wander?  Runs the trace build over every pair
 (in chunks), takes each block's pattern centres (every scoring pass: the points it tests lie
 within 2 of them), and reports the fraction of blocks whose centres leave a given compact
-visited-set window -- the blocks the compact-window kernel hands to its overflow pass.
+visited-set window -- the blocks a compact-window kernel would hand to an overflow pass (the
+round-2 experiment, commit 0a3ee45).
 
   python tools/excursion.py [--configs c3,c4] [--variant 0] [--out f.json]
 
-Window (px, py) = the bitmap geometry of DESIGN.md §4 "compact visited set": safe centres
-cx in [-px, px - 2], cy in [-py, py].
+Window (px, py): the bitmap layout of the full window over half-widths px x py (row length
+2px + 3, no border); the centres that keep every pattern point inside it are cx in
+[-px, px - 2], cy in [-py, py].
 """
 import argparse
 import json
