@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--no-fs", action="store_true")
+    ap.add_argument("--fs-pairs", type=int, default=4,
+                    help="pairs of the full-search side measurement (rank 0)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cmp", action="store_true", help="skip the comparison-BMA section")
@@ -505,7 +507,7 @@ def main():
 
     if rank == 0 and not args.no_fs:
         # FS (quality reference), same pairs, small sample: timed beside the path
-        nfs = min(n, 4)
+        nfs = min(n, max(1, args.fs_pairs))
         fsub = frames[:nfs]
         fo = me.alloc_outputs(nfs, cfg.nb, dev)
         me.me_fullsearch_batch(fsub, cfg.B, cfg.p, *fo)

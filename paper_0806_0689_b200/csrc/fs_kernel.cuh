@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(512)
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_key[64];
+    __shared__ unsigned long long s_stat[16][2];  // per-warp sums of SAD, SSE (one pair per CTA)
     uint8_t* smem = smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127);
     const int pair = blockIdx.y;
     const int tx = blockIdx.x % a.ntx, ty = blockIdx.x / a.ntx;
@@ -168,6 +169,7 @@ __global__ void __launch_bounds__(512)
     __syncthreads();
     // outputs + SSE at the FS MV (per-pair statistics), one warp per block
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned long long w_sad = 0, w_sse = 0;  // this warp's blocks (lane 0)
     for (int b = warp; b < nbt; b += nw) {
         const int lby = fdiv(b, r_tbx), lbx = b - lby * tbx_e;
         // centre first (reading C13): (0,0) is the MV unless another candidate is strictly
@@ -202,11 +204,23 @@ __global__ void __launch_bounds__(512)
             a.mv[g] = (uint32_t)(mdx & 0xffff) | ((uint32_t)mdy << 16);
             a.sad[g] = k2 >> 13;
             a.pts[g] = (uint16_t)(side * side);
-            if (a.stats) {
-                atomicAdd(&a.stats[pair * 3 + 0], (unsigned long long)(side * side));
-                atomicAdd(&a.stats[pair * 3 + 1], (unsigned long long)(k2 >> 13));
-                atomicAdd(&a.stats[pair * 3 + 2], (unsigned long long)sse);
+            w_sad += k2 >> 13;
+            w_sse += sse;
+        }
+    }
+    if (a.stats) {  // the CTA's sums first: 3 global atomics per CTA, not per block
+        if (lane == 0) {
+            s_stat[warp][0] = w_sad;
+            s_stat[warp][1] = w_sse;
+        }
+        __syncthreads();
+        if (threadIdx.x < 3) {
+            unsigned long long t = (unsigned long long)nbt * (unsigned long long)(side * side);
+            if (threadIdx.x > 0) {
+                t = 0;
+                for (int w = 0; w < nw; w++) t += s_stat[w][threadIdx.x - 1];
             }
+            atomicAdd(&a.stats[pair * 3 + threadIdx.x], t);
         }
     }
 }

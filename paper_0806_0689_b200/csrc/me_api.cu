@@ -170,8 +170,9 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
         a.bm_off = a.cur_off + TW * TH;
         a.init_off = a.bm_off + ((bm_bytes + 15) & ~15);
     }
-    // template words (initial bitmap, window border), tile counter, mbarrier (8-byte aligned)
-    L.smem = (size_t)((a.init_off + 8 * a.bm_words + 4 + 7) & ~7) + 8;  // 2 templates
+    // template words (initial bitmap, window border), tile counter, mbarrier (8-byte aligned),
+    // the warps' statistics sums (NW x 3 x 8 bytes)
+    L.smem = (size_t)((a.init_off + 8 * a.bm_words + 4 + 7) & ~7) + 8 + 24 * L.NW;  // 2 templates
     if (const char* e = getenv("ME_SMEM_PAD")) L.smem += (size_t)std::max(0, atoi(e));  // tuning only
     // L2 prefetch of the tile one resident wave ahead (ME_PF = distance in CTAs; tuning only):
     // measured slower on B200 (c3 1.442 -> 1.457 ms, c4 16.81 -> 18.79 ms at one wave), so off
