@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--no-fs", action="store_true")
-    ap.add_argument("--fs-pairs", type=int, default=4,
+    ap.add_argument("--fs-pairs", type=int, default=32,
                     help="pairs of the full-search side measurement (rank 0)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
