@@ -317,17 +317,25 @@ __global__ void __launch_bounds__(NWARP * 32)
         acc_sad = best;
         acc_sse = ss;
     }
-    if (a.stats) {
+    if (a.stats) {  // warp sums, then the CTA's: 3 global atomics per CTA (as dcds_kernel)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             acc_pts += __shfl_xor_sync(FULL, acc_pts, o);
             acc_sad += __shfl_xor_sync(FULL, acc_sad, o);
             acc_sse += __shfl_xor_sync(FULL, acc_sse, o);
         }
-        if (lane == 0 && acc_pts) {
-            atomicAdd(&a.stats[pair * 3 + 0], acc_pts);
-            atomicAdd(&a.stats[pair * 3 + 1], acc_sad);
-            atomicAdd(&a.stats[pair * 3 + 2], acc_sse);
+        unsigned long long* cs = reinterpret_cast<unsigned long long*>(bar + 1);  // [NWARP][3]
+        if (lane == 0) {
+            cs[3 * warp + 0] = acc_pts;
+            cs[3 * warp + 1] = acc_sad;
+            cs[3 * warp + 2] = acc_sse;
+        }
+        __syncthreads();  // (every warp of the CTA gets here)
+        if (threadIdx.x < 3) {
+            unsigned long long t = 0;
+#pragma unroll
+            for (int w = 0; w < NWARP; w++) t += cs[3 * w + threadIdx.x];
+            if (t) atomicAdd(&a.stats[pair * 3 + threadIdx.x], t);
         }
     }
 }

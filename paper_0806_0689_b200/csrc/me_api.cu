@@ -328,9 +328,10 @@ int run_bma(int alg, const uint8_t* cur0, const uint8_t* ref0, long long stride,
     const int groups = NW * 32 / G;
     a.cur_off = (pitch * a.rh + 127) & ~127;  // no slack needed (see plan_dcds)
     a.init_off = a.cur_off + ((std::max(TW * TH, (groups + 4) * a.bm_words * 4) + 15) & ~15);
-    // template words | row offsets (int4, 16-aligned) | row codes | mbarrier (8-aligned)
+    // template words | row offsets (int4, 16-aligned) | row codes | mbarrier (8-aligned) |
+    // the warps' statistics sums (NW x 3 x 8 bytes)
     const size_t tables = (size_t)((a.init_off + 4 * a.bm_words + 15) & ~15) + 16 * me::NROW + 4 * (me::NROW + (me::NROW & 1));
-    const size_t smem = tables + 8;
+    const size_t smem = tables + 8 + 24 * NW;
     if ((int)smem > g_smem_optin) return fail(ME_EINVAL, "tile does not fit in shared memory");
     CUtensorMap tc, tr;
     int rc = make_tmap(&tc, cur0, W, H, npairs, stride, TW, TH);
