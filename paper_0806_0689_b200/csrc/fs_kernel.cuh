@@ -40,7 +40,11 @@ struct FsArgs {
 // from the byte-phase copy (dx & 3) so they are aligned words; consecutive lanes take
 // consecutive dx, which the copy stride spreads over all 32 banks.  Per-block argmin:
 // shared-memory atomicMin on (SAD << 13 | rank) keys (reading C13).
-template <int B>
+// SIDE > 0 (with the region pitch PITCH): a build for one window size (2p + 1 = SIDE) whose
+// thread items sweep all SIDE + B - 1 rows of their dx column once -- every row loaded once
+// for up to B candidates, at immediate offsets from one base, each candidate's key formed as
+// its last row passes (at most B accumulators live).
+template <int B, int SIDE = 0, int PITCH = 0>
 __global__ void __launch_bounds__(512)
     fs_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
               const FsArgs a) {
@@ -116,6 +120,30 @@ __global__ void __launch_bounds__(512)
         const int col = (x0 + lbx * B - p - xs) + dxp;
         const uint32_t* base = sw + (col & 3) * cwords + (col >> 2) + (lby * B) * pw;
         uint32_t key = 0xffffffffu;
+        if constexpr (SIDE > 0) {
+            // candidate (dx, dy = d - p) block row i is region row y = d + i (from base); its
+            // key (SAD << 13) + rank, rank = 1 + d*SIDE + (dx + p): the d*SIDE part is added
+            // per candidate, 1 + dx + p once for the column
+            constexpr int PW = PITCH / 4;
+            uint32_t acc[SIDE];
+#pragma unroll
+            for (int y = 0; y < SIDE + B - 1; y++) {
+                uint32_t rw[W4];
+#pragma unroll
+                for (int w = 0; w < W4; w++) rw[w] = base[y * PW + w];
+#pragma unroll
+                for (int d = 0; d < SIDE; d++) {
+                    const int i = y - d;
+                    if (i >= 0 && i < B) {
+#pragma unroll
+                        for (int w = 0; w < W4; w++) acc[d] = vsad4(cw[i][w], rw[w], (i == 0 && w == 0) ? 0u : acc[d]);
+                        if (i == B - 1) key = min(key, (acc[d] << 13) + (uint32_t)(d * SIDE));
+                    }
+                }
+            }
+            atomicMin(&s_key[b], key + (uint32_t)(1 + dxp));
+            continue;
+        }
         const int c1 = min(a.nch, (sp + 1) * cps);
         for (int c = sp * cps; c < c1; c++) {
             const uint32_t* rb = base + (c * B) * pw;  // region row of (dy = c*B - p, i = 0)

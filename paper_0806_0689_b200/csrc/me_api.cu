@@ -414,8 +414,18 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
         const int t = atoi(e);
         if (t >= 64 && t <= 512 && t % 32 == 0) nthr = t;
     }
-    if (block == 16) me::fs_kernel<16><<<grid, nthr, smem, s>>>(tc, tr, a);
-    else me::fs_kernel<8><<<grid, nthr, smem, s>>>(tc, tr, a);
+    // the 8x8 +-16 build (c3) sweeps each dx column whole (fs_kernel SIDE), 4 warps per CTA
+    // (measured on B200, 32 c3 pairs: 1.375 ms at 128 threads, 1.415 at 256, 1.59 at 352;
+    // the chunked kernel 1.59 at 256; ME_FS_SWEEP=0 selects the chunked kernel)
+    const char* sw = getenv("ME_FS_SWEEP");
+    if (block == 8 && p == 16 && a.pitch == 128 && a.nsplit == 1 && !(sw && atoi(sw) == 0)) {
+        if (!getenv("ME_FS_THREADS")) nthr = 128;
+        me::fs_kernel<8, 33, 128><<<grid, nthr, smem, s>>>(tc, tr, a);
+    } else if (block == 16) {
+        me::fs_kernel<16><<<grid, nthr, smem, s>>>(tc, tr, a);
+    } else {
+        me::fs_kernel<8><<<grid, nthr, smem, s>>>(tc, tr, a);
+    }
     g_launches++;
     CK(cudaGetLastError());
     return ME_OK;
@@ -548,6 +558,7 @@ int me_init(int device) {
     if ((rc = allow_smem(me::mc_sse_tma_kernel<8>))) return rc;
     if ((rc = allow_smem(me::fs_kernel<16>))) return rc;
     if ((rc = allow_smem(me::fs_kernel<8>))) return rc;
+    if ((rc = allow_smem(me::fs_kernel<8, 33, 128>))) return rc;
     if (!g_scratch) CK(cudaMalloc(&g_scratch, 64));
     {  // visited-bitmap templates for every p (dcds_kernel.cuh, bm_template_word)
         static uint32_t tmpl[me::BM_TMPL_WORDS];
