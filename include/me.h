@@ -208,6 +208,15 @@ int me_dcds_batch_host(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_st
  * gpu_launches field). */
 int64_t me_launch_count(void);
 
+/* Blocks of the most recent DCDS / DCDS^S batch call (me_dcds_batch, me_dcds_s_batch,
+ * me_dcds_batch_packed, me_bma_batch with those algorithms) whose search left the compact
+ * visited set and was run again by the overflow pass (DESIGN.md §7 "Compact visited set":
+ * 16x16 blocks at p >= 26, or as ME_COMPACT forces); 0 when that call did not use the compact
+ * set.  Diagnostic only -- the outputs are the same either way.  *count_out is a HOST
+ * pointer; waits for that call's overflow passes, then reads the two list counts (interior and
+ * border blocks) from the device. */
+int me_dcds_overflow_count(uint64_t* count_out);
+
 /* Static description of the last error (never NULL). */
 const char* me_strerror(int status);
 

@@ -9,5 +9,5 @@ from .me import (  # noqa: F401
     ALGS, MEError, alloc_outputs, load, me_bma_batch, me_dcds, me_dcds_batch, me_dcds_batch_host, me_dcds_s_batch,
     me_fullsearch, me_fullsearch_batch, me_init, me_launch_count, me_mc_psnr, me_mc_sse_batch,
     me_quality_batch, me_set_stream, me_shutdown, me_ideal_nsp_map, me_mv_hist,
-    me_dcds_trace_batch, decode_trace, me_dcds_batch_packed,
+    me_dcds_trace_batch, decode_trace, me_dcds_batch_packed, me_dcds_overflow_count,
 )

@@ -71,6 +71,15 @@ struct SearchArgs {
     uint16_t* tlen;             // TRACE builds: [npairs][nb] passes of each block
     int tcap;
     int pf;                     // L2 prefetch distance in CTAs (0: none)
+    // visited-bitmap geometry (half-widths; = p unless compact) and the compact visited set of
+    // the B=16 ONE kernels (DESIGN.md §7 "Compact visited set"): a search whose centre leaves
+    // the compact window is abandoned and its block index (pair * nb + block) appended to ovf:
+    // [0] / [1] counts of interior / border blocks, [2] / [3] claim counters of the overflow
+    // passes, interior blocks at [4 + i], border blocks at [4 + ovf_cap - 1 - i]
+    int bmx, bmy;
+    int compact;
+    uint32_t* ovf;
+    uint32_t ovf_cap;  // npairs * nb
 };
 
 __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
@@ -177,6 +186,36 @@ __device__ __forceinline__ void ref_rows(const uint32_t* s, int o, int rstride,
     }
 }
 
+// ref_rows from GLOBAL memory (the overflow pass's interior blocks, rows W bytes apart, W a
+// multiple of 16): per row two 16-byte loads from the aligned chunk holding byte o, the W4 + 1
+// words at word offset (o >> 2) & 3 picked by two select levels, then the funnel shifts --
+// 2 vector loads per row where ref_rows issues W4 + 1 scalar ones (each scalar global load of a
+// warp touches one line per lane: the L1 tag rate bounds that pass).  Reads [o & ~15, +32).
+template <int R, int W4>
+__device__ __forceinline__ void ref_rows_gld(const uint32_t* s, int o, int rstride,
+                                             uint32_t (&out)[R][W4]) {
+    static_assert(W4 + 1 <= 6, "two 16-byte chunks cover W4 + 1 words at any word offset");
+    const int sh = o << 3, k = (o >> 2) & 3;
+    const uint4* b = reinterpret_cast<const uint4*>(s + ((o >> 2) & ~3));
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+        const uint4 v0 = b[r * (rstride >> 4)], v1 = b[r * (rstride >> 4) + 1];
+        const uint32_t v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        uint32_t u[6], wv[W4 + 1];
+#pragma unroll
+        for (int i = 0; i < 6; i++) u[i] = (k & 2) ? v[i + 2] : v[i];
+#pragma unroll
+        for (int w = 0; w <= W4; w++) wv[w] = (k & 1) ? u[w + 1] : u[w];
+#pragma unroll
+        for (int w = 0; w < W4; w++) out[r][w] = __funnelshift_r(wv[w], wv[w + 1], sh);
+    }
+}
+template <int R, int W4, bool GLD>
+__device__ __forceinline__ void ref_rows_any(const uint32_t* s, int o, int rstride, uint32_t (&out)[R][W4]) {
+    if constexpr (GLD) ref_rows_gld<R, W4>(s, o, rstride, out);
+    else ref_rows<R, W4>(s, o, rstride, out);
+}
+
 // W4+2 words around an ALIGNED row start a (a multiple of 4*W4 bytes: one vector load of
 // the row): w[0] = the word before, w[1..W4] = the row, w[W4+1] = the word after.
 template <int W4>
@@ -238,13 +277,23 @@ __device__ __forceinline__ int hcsp_dy(int k) { return k < 5 ? 0 : (k == 5 ? -1 
 // (reading C8; pattern offsets are at most 2) reads as "already visited" and is neither
 // scored nor counted -- the test-and-set is the whole feasibility test.
 // ----------------------------------------------------------------------------------------
-enum : int { ST_DONE = 0, ST_S1A = 1, ST_S3 = 3, ST_S4 = 4, ST_S4PRE = 5, ST_IDLE = 6 };
+enum : int { ST_DONE = 0, ST_S1A = 1, ST_S3 = 3, ST_S4 = 4, ST_S4PRE = 5, ST_IDLE = 6, ST_ESC = 7 };
+// (searching: ST_S1A <= st <= ST_S4PRE; ST_ESC: left the compact visited window)
 
 // Visited-bitmap geometry for window +-p: row length, words.  The bitmaps of a CTA's groups
 // are interleaved: word w of group gi at bms[w * (groups + 4) + gi], so the groups' test-and-
 // sets spread over the banks and the CTA initialises all bitmaps with dense stores.
 __host__ __device__ constexpr int bm_row(int p) { return 2 * p + 3; }
 __host__ __device__ constexpr int bm_nwords(int p) { return ((2 * p + 5) * bm_row(p) + 2 + 31) / 32; }
+// Compact visited set (the B=16 ONE kernels): the same layout over half-widths
+// bmx x bmy < p, no border (every bit is a point inside the +-p window), bit of (dx, dy) =
+// (dy+bmy+2)*(2bmx+3) + (dx+bmx+2).  A search may test points while its centre stays in
+// cx in [-bmx, bmx-2], cy in [-bmy, bmy] (pattern offsets are at most 2; the columns past
+// dx = bmx alias the next row); a centre moving out of that range ends the search (ST_ESC)
+// and the overflow pass (dcds_redo_kernel) searches the block again with the full bitmap.
+__host__ __device__ constexpr int bm_nwords_xy(int bmx, int bmy) {
+    return ((2 * bmy + 5) * (2 * bmx + 3) + 2 + 31) / 32;
+}
 
 
 // The two bitmap templates of window +-p (word t of the bordered bitmap): border bits set
@@ -277,7 +326,8 @@ __host__ __device__ constexpr int bm_tmpl_off(int p) {  // words before p's two 
 constexpr int BM_TMPL_WORDS = bm_tmpl_off(33);
 __constant__ uint32_t c_bm_tmpl[BM_TMPL_WORDS];
 
-template <int B, int G, bool TRACE = false>
+// GLD: the reference rows are read from global memory (ref_rows_gld), not shared memory.
+template <int B, int G, bool TRACE = false, bool GLD = false>
 struct GroupState {
     static constexpr int R = B / G;   // rows per lane (lane j of a group: rows j, j+G, ...)
     static constexpr int W4 = B / 4;  // 32-bit words per block row
@@ -321,14 +371,14 @@ struct GroupState {
         cidx += (kb & 1) ? de : -de;
     }
 
-    // centre (dx, dy) from its bitmap bit (the row length exceeds 2p + 1)
-    __device__ __forceinline__ void centre(int p, int& cx, int& cy) const {
-        const int bw = bm_row(p);
+    // centre (dx, dy) from its bitmap bit (bitmap half-widths bmx, bmy; row length 2bmx + 3)
+    __device__ __forceinline__ void centre(int bmx, int bmy, int& cx, int& cy) const {
+        const int bw = 2 * bmx + 3;
         // cidx / bw by a float quotient: cidx < 2^13 and the quotient stays >= 0.5/bw from an
         // integer, far above the error of the approximate division
         const int row = (int)__fdividef((float)cidx + 0.5f, (float)bw);
-        cy = row - p - 2;
-        cx = cidx - row * bw - p - 2;
+        cy = row - bmy - 2;
+        cx = cidx - row * bw - bmx - 2;
     }
 
     // Pattern steps of pid (ids above): HDSP d0 (2,0) d1 (0,1); VDSP (1,0) (0,2); middle points
@@ -366,11 +416,11 @@ struct GroupState {
     // Reset the group's visited bitmap (interleaved, word stride bst) to the border template
     // (skipped when the CTA initialised every bitmap) and enter Step 1.
     __device__ __forceinline__ void init_search(int j, uint32_t* bm, int bst, const uint32_t* bm_init,
-                                                int bm_words, int p, bool reset) {
+                                                int bm_words, int bmx, int bmy, bool reset) {
         if (reset)
             for (int w = j; w < bm_words; w += G) bm[w * bst] = bm_init[w];
-        const int bw = bm_row(p);
-        cidx = (p + 2) * bw + p + 2;
+        const int bw = 2 * bmx + 3;
+        cidx = (bmy + 2) * bw + bmx + 2;
         st = ST_S1A; pid = 0; kind = 0; pts = 0; want = 0xf;
     }
 
@@ -381,7 +431,7 @@ struct GroupState {
     // in Step 3 (switching strategy one) or, on the halfway stop, in a Step-4
     // state with no slots, which the next pass finishes.  All lanes of the warp call it (and
     // __syncwarp after it).
-    __device__ __forceinline__ void step1(const uint32_t* s, int j, int p, int pitch, int rstride,
+    __device__ __forceinline__ void step1(const uint32_t* s, int j, int p, int bw, int pitch, int rstride,
                                           int jrow) {
         const bool live = (st == ST_S1A);
         uint32_t sk[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -419,7 +469,6 @@ struct GroupState {
         }
         // visited set (reading C5): the HCSP points are already set in every group's initial
         // bitmap (the pattern sits at the window origin for every block)
-        const int bw = bm_row(p);
         pts = __popc(feas);
         best = key >> 3;
         trace(j, 15, feas, 0, 0);
@@ -440,7 +489,7 @@ struct GroupState {
     __device__ __forceinline__ uint32_t sse_rows(const uint32_t* s, int jrow, int rstride) const {
         uint32_t rw[R][W4];
         ME_CHECK(cpos + jrow >= 0 && cpos + jrow + (R - 1) * rstride + 4 * W4 + 4 <= dbg_region);
-        ref_rows<R, W4>(s, cpos + jrow, rstride, rw);
+        ref_rows_any<R, W4, GLD>(s, cpos + jrow, rstride, rw);
         uint32_t ss = 0;
 #pragma unroll
         for (int r = 0; r < R; r++)
@@ -451,9 +500,20 @@ struct GroupState {
 
     // One pass of the group's state machine; returns true when the block's search ended.
     // bm_win: the border-only template (the DCDS^S look-up's window test).
+    // bmx, bmy: bitmap half-widths; cpt: compact visited set (a centre leaving its range ends
+    // the search in ST_ESC).
     template <int VARIANT>
     __device__ __forceinline__ bool pass(const uint32_t* s, uint32_t* bm, int bst, const uint32_t* bm_win,
-                                         int j, int leader, int p, int pitch, int jrow, int rstride) {
+                                         int j, int leader, int bmx, int bmy, bool cpt, int pitch, int jrow,
+                                         int rstride) {
+        const int bw = 2 * bmx + 3;
+#ifdef ME_DEBUG
+        if (cpt && want) {  // compact set: the pattern's points stay inside the window
+            int dcx, dcy;
+            centre(bmx, bmy, dcx, dcy);
+            ME_CHECK(dcx >= -bmx && dcx <= bmx - 2 && dcy >= -bmy && dcy <= bmy);
+        }
+#endif
         // ---- visited-set test-and-set (reading C5): lane j of a group owns slots j, j+G, ...
         unsigned m4 = 0;
 #pragma unroll
@@ -486,7 +546,7 @@ struct GroupState {
                 uint32_t rw[R][W4];
                 ME_CHECK(((k & 1) ? o + db : o - db) >= 0 &&
                          ((k & 1) ? o + db : o - db) + (R - 1) * rstride + 4 * W4 + 4 <= dbg_region);
-                ref_rows<R, W4>(s, (k & 1) ? o + db : o - db, rstride, rw);
+                ref_rows_any<R, W4, GLD>(s, (k & 1) ? o + db : o - db, rstride, rw);
                 acc = 0;
 #pragma unroll
                 for (int r = 0; r < R; r++)
@@ -554,18 +614,23 @@ struct GroupState {
         int ccx = 0, ccy = 0;
         const int cpid = pid;
         const bool scoring = (st == ST_S3 || st == ST_S4);
-        if (TRACE) centre(p, ccx, ccy);
+        if (TRACE) centre(bmx, bmy, ccx, ccy);
         if (st != ST_S4PRE) pts += __popc(m4);
         if (st == ST_S3) {
             // Step 2 / Step 3
             if ((key >> 2) < best) {
                 best = key >> 2;
                 move(kb);
-                if ((kb >= 2) != (kind == 1)) { kind ^= 1; set_ddsp(kind, pitch, bm_row(p)); }  // near point
+                if ((kb >= 2) != (kind == 1)) { kind ^= 1; set_ddsp(kind, pitch, bw); }  // near point
+                if (cpt) {  // compact visited set: the next pattern must stay inside it
+                    int cx, cy;
+                    centre(bmx, bmy, cx, cy);
+                    if (cx < -bmx || cx > bmx - 2 || cy < -bmy || cy > bmy) { st = ST_ESC; want = 0; }
+                }
             } else {
                 st = VARIANT ? ST_S4PRE : ST_S4;  // BMP at the centre -> Step 4
-                if (VARIANT) set_distant(kind, pitch, bm_row(p));
-                else set_middle(kind, pitch, bm_row(p));
+                if (VARIANT) set_distant(kind, pitch, bw);
+                else set_middle(kind, pitch, bw);
                 want = 3;
             }
         } else if (VARIANT && st == ST_S4PRE) {
@@ -575,7 +640,7 @@ struct GroupState {
             const uint32_t dp = (m4 & 2) ? (v01 >> 16) : 0xffffffffu;
             want = (dp < dn) ? 2 : 1;
             st = ST_S4;
-            set_middle(kind, pitch, bm_row(p));
+            set_middle(kind, pitch, bw);
         } else if (st == ST_S4) {
             // Step 4: strict minimum of the middle points against the centre
             if ((key >> 2) < best) {
@@ -590,13 +655,38 @@ struct GroupState {
     }
 };
 
+// The outputs of block gblk (index pair * nb + block): MV, SAD, NSP.
+__device__ __forceinline__ void store_block(const SearchArgs& a, long long gblk, int cx, int cy,
+                                            uint32_t best, int pts) {
+    if (a.packed) {  // 6-byte records: int8 (dx, dy), 16-bit SAD (<= 255*256), NSP
+        reinterpret_cast<uint16_t*>(a.mv)[gblk] = (uint16_t)((cx & 0xff) | ((cy & 0xff) << 8));
+        reinterpret_cast<uint16_t*>(a.sad)[gblk] = (uint16_t)best;
+    } else {
+        a.mv[gblk] = (uint32_t)(cx & 0xffff) | ((uint32_t)cy << 16);
+        a.sad[gblk] = best;
+    }
+    a.pts[gblk] = (uint16_t)pts;
+}
+
+// Overflow pass (below): an interior block's +-p window and the row loads' over-read lie inside
+// the frame's rows, so it reads the reference frame directly.
+__device__ __forceinline__ bool redo_interior(const SearchArgs& a, long long gblk) {
+    const int blk = (int)(gblk % a.nb), by = blk / a.nbx, bx = blk - by * a.nbx;
+    const int B = a.W / a.nbx, x0 = bx * B, y0 = by * B;
+    // (ref_rows_gld reads [o & ~15, +32) for a candidate at column o: x0 - p - 15 >= 0 and
+    // x0 + p + 32 <= W keep every read inside the window's own rows)
+    return x0 >= a.p + 15 && x0 + a.p + 32 <= a.W && y0 >= a.p && y0 + B + a.p <= a.H;
+}
+
 // ONE: the tile holds at most one block per lane group (the default geometries: 16x4 blocks
 // for 64 groups at B=8, 8x4 for 32 groups at B=16) -- every group takes its block at the
 // start, keeps the finished search in registers, and the SSE and outputs of all blocks are
 // produced in one dense phase after the last search ends.  Otherwise blocks are handed out
 // from a tile counter as groups finish.
-template <int B, int G, int NWARP, int VARIANT, bool TRACE = false, bool ONE = false, int PITCH = 0>
-__global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
+// CPT: the compact-visited-set build of the 16x16 ONE kernel (5 CTAs per SM: <= 48 registers).
+template <int B, int G, int NWARP, int VARIANT, bool TRACE = false, bool ONE = false, int PITCH = 0,
+          bool CPT = false>
+__global__ void __launch_bounds__(NWARP * 32, ONE ? (B == 8 ? 36 / NWARP : (CPT ? 5 : 1)) : 1)
     dcds_kernel(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_ref,
                 const SearchArgs a) {
     static_assert(G == 1 || G == 2 || G == 4 || G == 8 || G == 16, "lane-group size");
@@ -614,6 +704,10 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
     const int xs = (x0 - a.p) & ~15;  // floor to 16 (two's complement)
     const int ys = y0 - a.p;
     const int pitch = PITCH ? PITCH : a.pitch, p = a.p;
+    // compact visited set: the B=16 ONE kernels (4-8x8 tiles at +-32 need 5 CTAs/SM)
+    constexpr bool CPT_OK = CPT && ONE && B == 16 && !TRACE;
+    const bool cpt = CPT_OK && a.compact;
+    const int bmx = CPT_OK ? a.bmx : p, bmy = CPT_OK ? a.bmy : p;
 
     // shared layout: reference region (pitch x rh) | current tile (TW x TH) | group bitmaps |
     // bitmap template | tile counter | mbarrier | per-warp statistics sums (NWARP x 3 u64).  ONE kernels overlay the bitmaps on the current tile,
@@ -652,11 +746,23 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
             }
         }
     }
-    const int bw = bm_row(p);
-    // bitmap templates (border only / border + HCSP), precomputed in constant memory
+    const int bw = 2 * bmx + 3;
+    // bitmap templates (border only / border + HCSP), precomputed in constant memory; the
+    // compact set has no border (no bits / the 7 HCSP bits)
     for (int t = threadIdx.x; t < a.bm_words; t += NWARP * 32) {
-        bm_win[t] = c_bm_tmpl[bm_tmpl_off(p) + t];
-        bm_init[t] = c_bm_tmpl[bm_tmpl_off(p) + a.bm_words + t];
+        if (cpt) {
+            const int c = (bmy + 2) * bw + bmx + 2;
+            const int hc[7] = {c, c - 1, c + 1, c - 2, c + 2, c - bw, c + bw};
+            uint32_t w = 0;
+#pragma unroll
+            for (int k = 0; k < 7; k++)
+                if ((hc[k] >> 5) == t) w |= 1u << (hc[k] & 31);
+            bm_win[t] = 0;
+            bm_init[t] = w;
+        } else {
+            bm_win[t] = c_bm_tmpl[bm_tmpl_off(p) + t];
+            bm_init[t] = c_bm_tmpl[bm_tmpl_off(p) + a.bm_words + t];
+        }
     }
     mbar_wait(bar, 0);
     if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
@@ -688,15 +794,8 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
     };
     auto output = [&](uint32_t ss) {
         int cx, cy;
-        gs.centre(p, cx, cy);
-        if (a.packed) {  // 6-byte records: int8 (dx, dy), 16-bit SAD (<= 255*256), NSP
-            reinterpret_cast<uint16_t*>(a.mv)[gblk] = (uint16_t)((cx & 0xff) | ((cy & 0xff) << 8));
-            reinterpret_cast<uint16_t*>(a.sad)[gblk] = (uint16_t)gs.best;
-        } else {
-            a.mv[gblk] = (uint32_t)(cx & 0xffff) | ((uint32_t)cy << 16);
-            a.sad[gblk] = gs.best;
-        }
-        a.pts[gblk] = (uint16_t)gs.pts;
+        gs.centre(bmx, bmy, cx, cy);
+        store_block(a, gblk, cx, cy, gs.best, gs.pts);
         if (TRACE) a.tlen[gblk] = (uint16_t)gs.npass;
         acc_pts += (unsigned)gs.pts;
         acc_sad += gs.best;
@@ -714,21 +813,28 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
             reinterpret_cast<uint4*>(bms)[e] = make_uint4(v, v, v, v);
         }
         __syncthreads();
-        if (have) gs.init_search(j, bm, BST, bm_init, a.bm_words, p, false);
+        if (have) gs.init_search(j, bm, BST, bm_init, a.bm_words, bmx, bmy, false);
         else { gs.st = ST_IDLE; gs.want = 0; }
         if (__any_sync(FULL, have)) {
-            gs.step1(s, j, p, pitch, rstride, jrow);
+            gs.step1(s, j, p, bw, pitch, rstride, jrow);
             __syncwarp();  // the visited bits are set before the pass tests them
-            while (__any_sync(FULL, gs.st != ST_DONE && gs.st != ST_IDLE))
-                if (gs.template pass<VARIANT>(s, bm, BST, bm_win, j, leader, p, pitch, jrow, rstride)) {
+            while (__any_sync(FULL, gs.st != ST_DONE && gs.st < ST_IDLE))
+                if (gs.template pass<VARIANT>(s, bm, BST, bm_win, j, leader, bmx, bmy, cpt, pitch, jrow,
+                                              rstride)) {
                     gs.st = ST_DONE; gs.want = 0;
                 }
             // every search of the warp ended: SSE of the compensated blocks (P:342 aspect 4)
-            // and the outputs, in one dense phase
-            uint32_t ss = have ? gs.sse_rows(s, jrow, rstride) : 0u;
+            // and the outputs, in one dense phase (a search that left the compact visited set
+            // hands its block to the overflow pass instead)
+            const bool live = have && (!CPT_OK || gs.st != ST_ESC);
+            uint32_t ss = live ? gs.sse_rows(s, jrow, rstride) : 0u;
 #pragma unroll
             for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
-            if (have && j == 0) output(ss);
+            if (live && j == 0) output(ss);
+            if (CPT_OK && have && !live && j == 0) {
+                if (redo_interior(a, gblk)) a.ovf[4 + atomicAdd(&a.ovf[0], 1u)] = (uint32_t)gblk;
+                else a.ovf[4 + a.ovf_cap - 1 - atomicAdd(&a.ovf[1], 1u)] = (uint32_t)gblk;
+            }
         }
     } else for (;;) {
         // ---- groups that are done take the next block of the tile
@@ -747,7 +853,7 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
                 if (need) {
                     if (idx < nbt) {
                         take(idx);
-                        gs.init_search(j, bm, BST, bm_init, a.bm_words, p, true);
+                        gs.init_search(j, bm, BST, bm_init, a.bm_words, bmx, bmy, true);
                     } else {
                         gs.st = ST_IDLE; gs.want = 0;
                     }
@@ -758,11 +864,12 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
         if (__all_sync(FULL, gs.st == ST_IDLE)) break;
         // ---- groups that just took a block run Step 1 in one straight-line step
         if (__any_sync(FULL, gs.st == ST_S1A)) {
-            gs.step1(s, j, p, pitch, rstride, jrow);
+            gs.step1(s, j, p, bw, pitch, rstride, jrow);
             __syncwarp();  // the visited bits are set before the pass tests them
         }
 
-        const bool fin = gs.template pass<VARIANT>(s, bm, BST, bm_win, j, leader, p, pitch, jrow, rstride);
+        const bool fin = gs.template pass<VARIANT>(s, bm, BST, bm_win, j, leader, bmx, bmy, false, pitch,
+                                                   jrow, rstride);
 
         // ---- finished blocks: SSE of the compensated block (P:342 aspect 4), outputs
         if (__any_sync(FULL, fin)) {
@@ -807,6 +914,130 @@ __global__ void __launch_bounds__(NWARP * 32, (ONE && B == 8) ? 36 / NWARP : 1)
             for (int w = 0; w < NWARP; w++) t += cs[3 * w + threadIdx.x];
             atomicAdd(&a.stats[pair * 3 + threadIdx.x], t);
         }
+    }
+}
+
+// ---- overflow passes of the compact visited set (DESIGN.md §7 "Compact visited set") ----
+// Every block whose search left the compact window (SearchArgs::ovf) is searched again from
+// the start by the same GroupState code with the full +-p bitmap (border template), so its
+// outputs are those of the full-bitmap kernels.  One block per lane group, groups claiming
+// blocks from the list.  GLOBAL: the interior blocks, reading the reference frame directly
+// (region base = the frame row y0 - p, pitch W; no shared staging, so 32 warps per SM);
+// otherwise the border blocks, one warp per CTA, each group staging its block's (B + 2p) x
+// redo_pitch window by cp.async with edge replication (reading C9, as fixup_edges).
+__host__ __device__ constexpr int redo_pitch(int B, int p) {
+    // the main kernel's bound for a one-block tile (TW + 2p + 31 bytes), 16 * odd bytes
+    const int w = (B + 2 * p + 31 + 15) & ~15;
+    return ((w >> 4) & 1) ? w : w + 16;
+}
+__host__ __device__ constexpr int redo_smem(int B, int G, int p, bool global, int nwarps) {
+    return (global ? 0 : nwarps * (32 / G) * redo_pitch(B, p) * (B + 2 * p)) +
+           (2 + nwarps * (32 / G)) * bm_nwords(p) * 4;
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+template <int B, int G, int VARIANT, bool GLOBAL>
+__global__ void __launch_bounds__(GLOBAL ? 128 : 32, GLOBAL ? 8 : 1) dcds_redo_kernel(const SearchArgs a) {
+    constexpr int NG = 32 / G;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane % G, g = lane / G, leader = g * G, slot = warp * NG + g;
+    const int nslots = (blockDim.x >> 5) * NG;
+    const int p = a.p, W = a.W, H = a.H;
+    const int rp = GLOBAL ? W : redo_pitch(B, p), rr = B + 2 * p;
+    const int words = bm_nwords(p);
+    // shared: staged windows (border pass) | templates (border + HCSP, border only) | bitmaps
+    uint8_t* region = smem + (GLOBAL ? 0 : slot * rp * rr);
+    uint32_t* bm_init = reinterpret_cast<uint32_t*>(smem + (GLOBAL ? 0 : nslots * rp * rr));
+    uint32_t* bm_win = bm_init + words;
+    uint32_t* bm = bm_win + words + slot * words;
+    for (int t = threadIdx.x; t < words; t += blockDim.x) {
+        bm_win[t] = c_bm_tmpl[bm_tmpl_off(p) + t];
+        bm_init[t] = c_bm_tmpl[bm_tmpl_off(p) + words + t];
+    }
+    __syncthreads();
+    const uint32_t count = a.ovf[GLOBAL ? 0 : 1];
+    uint32_t* claim = &a.ovf[GLOBAL ? 2 : 3];
+    const int rstride = G * rp, jrow = j * rp;
+    GroupState<B, G, false, GLOBAL> gs;
+    for (;;) {
+        uint32_t e = 0xffffffffu;
+        if (j == 0) e = atomicAdd(claim, 1u);
+        e = __shfl_sync(FULL, e, leader);
+        const bool have = e < count;
+        if (!__any_sync(FULL, have)) break;
+        long long gblk = 0;
+        int pair = 0, x0 = 0, y0 = 0, xs = 0;
+        const uint32_t* s = reinterpret_cast<const uint32_t*>(region);
+        const uint8_t* ref = a.ref0;
+        if (have) {
+            gblk = a.ovf[GLOBAL ? 4 + e : 4 + a.ovf_cap - 1 - e];
+            pair = (int)(gblk / a.nb);
+            const int blk = (int)(gblk - (long long)pair * a.nb);
+            const int by = blk / a.nbx, bx = blk - by * a.nbx;
+            x0 = bx * B;
+            y0 = by * B;
+            ref += (long long)pair * a.stride;
+            xs = (x0 - p) & ~15;
+            if constexpr (GLOBAL) {
+                s = reinterpret_cast<const uint32_t*>(ref + (long long)(y0 - p) * W);
+            } else {
+                // xs and W are multiples of 16: a 16-byte chunk is wholly inside or outside the
+                // frame; rows clamp to the frame, in-frame chunks by cp.async, then (below) the
+                // out-of-frame chunks replicate the row's edge byte
+                for (int q = j; q < rr * (rp >> 4); q += G) {
+                    const int i = q / (rp >> 4), x = xs + 16 * (q - i * (rp >> 4));
+                    if (x >= 0 && x + 16 <= W)
+                        cp_async16(region + i * rp + (x - xs), ref + (long long)min(max(y0 - p + i, 0), H - 1) * W + x);
+                }
+            }
+        }
+        if constexpr (!GLOBAL) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();  // every lane of the warp: the copies of the whole group are visible
+            if (have)
+                for (int q = j; q < rr * (rp >> 4); q += G) {
+                    const int i = q / (rp >> 4), x = xs + 16 * (q - i * (rp >> 4));
+                    if (x < 0 || x + 16 > W) {
+                        const uint32_t e4 = region[i * rp + (x < 0 ? -xs : W - 1 - xs)] * 0x01010101u;
+                        *reinterpret_cast<uint4*>(region + i * rp + (x - xs)) = make_uint4(e4, e4, e4, e4);
+                    }
+                }
+        }
+        if (have) {
+            const int origin = GLOBAL ? p * W + x0 : p * rp + (x0 - xs);
+            gs.load_cur(origin, a.cur0 + (long long)pair * a.stride + (long long)y0 * W + x0, W, j);
+#ifdef ME_DEBUG
+            gs.dbg_region = rp * rr;
+            gs.dbg_bits = 32 * words;
+#endif
+            gs.init_search(j, bm, 1, bm_init, words, p, p, true);
+        } else {
+            gs.st = ST_IDLE; gs.want = 0;
+        }
+        __syncwarp();  // the staged windows and bitmaps are visible to the group
+        gs.step1(s, j, p, bm_row(p), rp, rstride, jrow);
+        __syncwarp();
+        while (__any_sync(FULL, gs.st != ST_DONE && gs.st < ST_IDLE))
+            if (gs.template pass<VARIANT>(s, bm, 1, bm_win, j, leader, p, p, false, rp, jrow, rstride)) {
+                gs.st = ST_DONE; gs.want = 0;
+            }
+        uint32_t ss = have ? gs.sse_rows(s, jrow, rstride) : 0u;
+#pragma unroll
+        for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
+        if (have && j == 0) {
+            int cx, cy;
+            gs.centre(p, p, cx, cy);
+            store_block(a, gblk, cx, cy, gs.best, gs.pts);
+            if (a.stats) {
+                atomicAdd(&a.stats[pair * 3 + 0], (unsigned long long)gs.pts);
+                atomicAdd(&a.stats[pair * 3 + 1], (unsigned long long)gs.best);
+                atomicAdd(&a.stats[pair * 3 + 2], (unsigned long long)ss);
+            }
+        }
+        __syncwarp();  // every lane is done with the windows before the next blocks replace them
     }
 }
 

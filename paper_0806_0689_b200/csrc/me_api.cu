@@ -29,7 +29,16 @@ unsigned long long* g_scratch = nullptr;  // device u64 scratch (me_mc_psnr)
 char g_err[512] = "";
 long long g_launches = 0;
 int g_smem_optin = 0;
+int g_smem_sm = 233472;  // shared memory per SM (bytes)
 int g_sms = 148;
+// overflow list of the compact visited set (SearchArgs::ovf; grow-only, 4 bytes per block)
+uint8_t* g_ovf = nullptr;
+size_t g_ovf_cap = 0;
+bool g_ovf_used = false;  // the last DCDS batch call used the compact set
+// the list is one buffer: a compact call on another stream than the previous one waits for it
+cudaEvent_t g_ovf_ev = nullptr;
+cudaStream_t g_ovf_stream = nullptr;
+int grow(uint8_t** p, size_t* cap, size_t need);
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;  // driver entry point (no -lcuda)
 
 // grow-only staging buffers of me_dcds_batch_host (two sets for double buffering)
@@ -104,7 +113,7 @@ struct DcdsLaunch {
 
 // Launch geometry: lane-group size G, tile of tbx x tby blocks.
 // ME_G / ME_TILE=tbx,tby override the defaults (tuning only).
-DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
+DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs, bool allow_compact = false) {
     DcdsLaunch L;
     me::SearchArgs& a = L.a;
     const int nbx = W / B, nby = H / B;
@@ -162,17 +171,48 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs) {
     L.TW = TW; L.TH = TH;
     // the ONE kernels (one block per lane group) exist for the default geometry
     L.one = tbx * tby <= groups && L.G == (B == 16 ? 8 : 2) && (L.NW == (B == 16 ? 8 : 4) || (B == 8 && L.NW == 8));
-    const int bm_bytes = (groups + 4) * a.bm_words * 4;  // interleaved, word stride groups + 4
-    if (L.one) {  // bitmaps overlay the current tile (read into registers first)
-        a.bm_off = a.cur_off;
-        a.init_off = a.cur_off + ((std::max(TW * TH, bm_bytes) + 15) & ~15);
-    } else {
-        a.bm_off = a.cur_off + TW * TH;
-        a.init_off = a.bm_off + ((bm_bytes + 15) & ~15);
+    auto layout = [&](int words) {  // bitmaps, templates, counter, mbarrier; returns the bytes
+        const int bm_bytes = (groups + 4) * words * 4;  // interleaved, word stride groups + 4
+        if (L.one) {  // bitmaps overlay the current tile (read into registers first)
+            a.bm_off = a.cur_off;
+            a.init_off = a.cur_off + ((std::max(TW * TH, bm_bytes) + 15) & ~15);
+        } else {
+            a.bm_off = a.cur_off + TW * TH;
+            a.init_off = a.bm_off + ((bm_bytes + 15) & ~15);
+        }
+        // template words (initial bitmap, window border), tile counter, mbarrier (8-aligned),
+        // the warps' statistics sums (NW x 3 x 8 bytes)
+        return (size_t)((a.init_off + 8 * words + 4 + 7) & ~7) + 8 + 24 * L.NW;  // 2 templates
+    };
+    a.bmx = a.bmy = p;
+    a.compact = 0;
+    a.ovf = nullptr;
+    L.smem = layout(a.bm_words);
+    // Compact visited set (B=16 ONE kernels): at +-32 the bitmaps (145 words per
+    // group) hold the CTA to 4 per SM; a 51 x 45 window (bmx 24, bmy 20: 72 words) fits 5, and
+    // 0.14 % of c4's searches leave it (tools/excursion.py, profiles/r2/excursion.json) -- the
+    // overflow pass searches those again.  Used where it raises the CTAs per SM (the ONE
+    // kernels' launch bound is 5); ME_COMPACT=0 disables it, ME_COMPACT=bmx,bmy forces a
+    // window (tests: 4 <= bmx, 2 <= bmy, both <= p - 2).
+    if (allow_compact && L.one && B == 16) {
+        int cx = 0, cy = 0;
+        const char* e = getenv("ME_COMPACT");
+        if (e && sscanf(e, "%d,%d", &cx, &cy) == 2) {
+            if (cx < 4 || cy < 2 || cx > p - 2 || cy > p - 2) cx = cy = 0;
+        } else if (!(e && atoi(e) == 0) && p >= 26) {
+            cx = std::min(24, p - 2);
+            cy = std::min(20, p - 2);
+            auto ctas = [](size_t b) { return std::min(5, g_smem_sm / ((int)b + 1024)); };
+            if (ctas(layout(me::bm_nwords_xy(cx, cy))) <= ctas(L.smem)) cx = cy = 0;
+        }
+        if (cx > 0) {
+            a.bmx = cx;
+            a.bmy = cy;
+            a.compact = 1;
+            a.bm_words = me::bm_nwords_xy(cx, cy);
+        }
+        L.smem = layout(a.bm_words);
     }
-    // template words (initial bitmap, window border), tile counter, mbarrier (8-byte aligned),
-    // the warps' statistics sums (NW x 3 x 8 bytes)
-    L.smem = (size_t)((a.init_off + 8 * a.bm_words + 4 + 7) & ~7) + 8 + 24 * L.NW;  // 2 templates
     if (const char* e = getenv("ME_SMEM_PAD")) L.smem += (size_t)std::max(0, atoi(e));  // tuning only
     // L2 prefetch of the tile one resident wave ahead (ME_PF = distance in CTAs; tuning only):
     // measured slower on B200 (c3 1.442 -> 1.457 ms, c4 16.81 -> 18.79 ms at one wave), so off
@@ -195,6 +235,15 @@ void launch_dcds_t(const DcdsLaunch& L, const CUtensorMap& tc, const CUtensorMap
             // the bench geometries (B=8: 16x4 tiles, +-16; B=16: 4x8 tiles, +-32) also exist
             // with the region pitch as a constant (immediate row offsets in the loads)
             constexpr int PC = B == 16 ? 176 : 192;
+            if constexpr (B == 16) {
+                if (L.a.compact) {  // the compact-visited-set builds (5 CTAs per SM)
+                    if (L.a.pitch == PC)
+                        me::dcds_kernel<B, G, DNW, VARIANT, false, true, PC, true><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
+                    else
+                        me::dcds_kernel<B, G, DNW, VARIANT, false, true, 0, true><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
+                    return;
+                }
+            }
             if (L.a.pitch == PC)
                 me::dcds_kernel<B, G, DNW, VARIANT, false, true, PC><<<L.grid, DNW * 32, L.smem, s>>>(tc, tr, L.a);
             else
@@ -256,8 +305,24 @@ int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npa
              int block, int p, int16_t* mv, uint32_t* sad, uint16_t* pts, uint64_t* stats,
              int variant, cudaStream_t s, uint64_t* trace = nullptr, uint16_t* tlen = nullptr,
              int tcap = 0, bool packed = false) {
-    DcdsLaunch L = plan_dcds(W, H, block, p, npairs);
+    // the compact visited set's overflow list holds 32-bit block indices
+    const bool compact_ok = !trace && (long long)npairs * (W / block) * (H / block) < (1ll << 31);
+    DcdsLaunch L = plan_dcds(W, H, block, p, npairs, compact_ok);
     if ((int)L.smem > g_smem_optin) return fail(ME_EINVAL, "tile does not fit in shared memory");
+    if (L.a.compact) {
+        L.a.ovf_cap = (uint32_t)((long long)npairs * L.a.nb);
+        int rc = grow(&g_ovf, &g_ovf_cap, 4 * (4 + (size_t)L.a.ovf_cap));
+        if (rc) return rc;
+        L.a.ovf = reinterpret_cast<uint32_t*>(g_ovf);
+        if (g_ovf_stream && g_ovf_stream != s) {
+            // (not while s is being captured into a graph: its replays are ordered by the user)
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            CK(cudaStreamIsCapturing(s, &cs));
+            if (cs == cudaStreamCaptureStatusNone) CK(cudaStreamWaitEvent(s, g_ovf_ev, 0));
+        }
+        CK(cudaMemsetAsync(g_ovf, 0, 16, s));
+    }
+    g_ovf_used = L.a.compact != 0;
     if (trace && !(L.G == (block == 16 ? 8 : 2) && L.NW == (block == 16 ? 8 : 4)))
         return fail(ME_EINVAL, "trace builds exist for the default lane-group geometry only (unset ME_G/ME_NW)");
     L.a.trace = trace; L.a.tlen = tlen; L.a.tcap = tcap;
@@ -278,6 +343,24 @@ int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npa
         else launch_dcds_trace<8, 2, 4>(L, variant, tc, tr, s);
     } else if (block == 16) {
         if (variant) launch_dcds_b<16, 1>(L, tc, tr, s); else launch_dcds_b<16, 0>(L, tc, tr, s);
+        if (L.a.compact) {
+            // overflow passes (persistent grids): interior blocks from global memory (4 warps
+            // per CTA, 8 CTAs per SM), border blocks staged (one warp per CTA)
+            CK(cudaGetLastError());
+            g_launches += 2;
+            const int gs_ = me::redo_smem(16, 8, p, true, 4), bs_ = me::redo_smem(16, 8, p, false, 1);
+            const dim3 gg(g_sms * 8), bg(g_sms * std::max(1, std::min(32, g_smem_sm / (bs_ + 1024))));
+            if (variant) {
+                me::dcds_redo_kernel<16, 8, 1, true><<<gg, 128, gs_, s>>>(L.a);
+                me::dcds_redo_kernel<16, 8, 1, false><<<bg, 32, bs_, s>>>(L.a);
+            } else {
+                me::dcds_redo_kernel<16, 8, 0, true><<<gg, 128, gs_, s>>>(L.a);
+                me::dcds_redo_kernel<16, 8, 0, false><<<bg, 32, bs_, s>>>(L.a);
+            }
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(g_ovf_ev, s));
+            g_ovf_stream = s;
+        }
     } else {
         if (variant) launch_dcds_b<8, 1>(L, tc, tr, s); else launch_dcds_b<8, 0>(L, tc, tr, s);
     }
@@ -520,6 +603,7 @@ int me_init(int device) {
         return ME_ECUDA;
     }
     g_smem_optin = (int)prop.sharedMemPerBlockOptin;
+    g_smem_sm = (int)prop.sharedMemPerMultiprocessor;
     g_sms = prop.multiProcessorCount;
     int rc;
 #define ME_ALLOW(B, G, V) \
@@ -538,6 +622,14 @@ int me_init(int device) {
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, false, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true, 176, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true, 176, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, false, true, 0, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 1, false, true, 0, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_redo_kernel<16, 8, 0, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_redo_kernel<16, 8, 1, true>))) return rc;
+    if ((rc = allow_smem(me::dcds_redo_kernel<16, 8, 0, false>))) return rc;
+    if ((rc = allow_smem(me::dcds_redo_kernel<16, 8, 1, false>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 0, true, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<8, 2, 4, 1, true, true>))) return rc;
     if ((rc = allow_smem(me::dcds_kernel<16, 8, 8, 0, true, true>))) return rc;
@@ -580,6 +672,7 @@ int me_init(int device) {
     for (auto& cs : g_copy_streams)
         if (!cs) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     if (!g_order_ev) CK(cudaEventCreateWithFlags(&g_order_ev, cudaEventDisableTiming));
+    if (!g_ovf_ev) CK(cudaEventCreateWithFlags(&g_ovf_ev, cudaEventDisableTiming));
     for (auto& st : g_stage) {  // me_dcds_batch_host staging: allocated here, not per call
         if ((rc = grow(&st.frames, &st.frames_cap, (size_t)kStageFrames))) return rc;
         if ((rc = grow(&st.out, &st.out_cap, (size_t)kStageFrames / 4))) return rc;  // >= outputs of a full chunk
@@ -829,6 +922,18 @@ int me_dcds_batch_host(const uint8_t* cur0, const uint8_t* ref0, int64_t pair_st
 
 int64_t me_launch_count(void) { return g_launches; }
 
+int me_dcds_overflow_count(uint64_t* count_out) {
+    if (!count_out) return fail(ME_EINVAL, "NULL count_out");
+    if (g_dev < 0) return fail(ME_ENOTINIT, "me_init has not succeeded");
+    uint32_t c[2] = {0, 0};  // interior + border blocks
+    if (g_ovf_used) {
+        CK(cudaEventSynchronize(g_ovf_ev));
+        CK(cudaMemcpy(c, g_ovf, 8, cudaMemcpyDeviceToHost));
+    }
+    *count_out = (uint64_t)c[0] + c[1];
+    return ME_OK;
+}
+
 const char* me_strerror(int status) {
     switch (status) {
         case ME_OK: return "ok";
@@ -850,6 +955,13 @@ void me_shutdown(void) {
     }
     if (g_scratch) cudaFree(g_scratch);
     g_scratch = nullptr;
+    if (g_ovf) cudaFree(g_ovf);
+    g_ovf = nullptr;
+    g_ovf_cap = 0;
+    g_ovf_used = false;
+    if (g_ovf_ev) cudaEventDestroy(g_ovf_ev);
+    g_ovf_ev = nullptr;
+    g_ovf_stream = nullptr;
     for (auto& cs : g_copy_streams) {
         if (cs) cudaStreamDestroy(cs);
         cs = nullptr;

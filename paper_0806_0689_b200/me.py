@@ -23,6 +23,7 @@ SYMBOLS = (
     "me_dcds_s_batch", "me_fullsearch_batch", "me_mc_sse_batch", "me_dcds_batch_host",
     "me_launch_count", "me_strerror", "me_shutdown", "me_quality_batch", "me_bma_batch",
     "me_ideal_nsp_map", "me_mv_hist", "me_dcds_trace_batch", "me_dcds_batch_packed",
+    "me_dcds_overflow_count",
 )
 
 # me_alg ids (include/me.h)
@@ -66,6 +67,7 @@ def load() -> ctypes.CDLL:
     L.me_ideal_nsp_map.argtypes = [i32, i32, vp, vp, vp]
     L.me_mv_hist.argtypes = [vp, i64, i32, vp]
     L.me_dcds_trace_batch.argtypes = [i32] + batch[:-1] + [vp, i32, vp]
+    L.me_dcds_overflow_count.argtypes = [vp]
     L.me_launch_count.argtypes = []
     L.me_launch_count.restype = i64
     L.me_strerror.argtypes = [i32]
@@ -254,6 +256,14 @@ def me_quality_batch(mv, mv_fs, out=None):
         out = torch.empty(n, 2, dtype=torch.float64, device=mv.device)
     _check(load().me_quality_batch(_ptr(mv), _ptr(mv_fs), n, nb, _ptr(out)))
     return out
+
+
+def me_dcds_overflow_count() -> int:
+    """Blocks of the last DCDS / DCDS^S batch that the compact visited set handed to the
+    overflow pass (include/me.h; 0 when that call did not use the compact set)."""
+    n = ctypes.c_uint64()
+    _check(load().me_dcds_overflow_count(ctypes.byref(n)))
+    return n.value
 
 
 def me_launch_count() -> int:

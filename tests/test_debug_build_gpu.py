@@ -25,7 +25,8 @@ def test_parity_suites_under_debug_checks():
     assert chk.stdout.strip().endswith("libme_debug.so"), chk.stdout + chk.stderr
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_geometry_gpu.py"),
-                        os.path.join(ROOT, "tests", "test_trace_gpu.py")],
+                        os.path.join(ROOT, "tests", "test_trace_gpu.py"),
+                        os.path.join(ROOT, "tests", "test_compact_gpu.py")],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "passed" in r.stdout

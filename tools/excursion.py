@@ -1,8 +1,8 @@
 """How far do the DCDS searches of a config wander?  Runs the trace build over every pair
 (in chunks), takes each block's pattern centres (every scoring pass: the points it tests lie
 within 2 of them), and reports the fraction of blocks whose centres leave a given compact
-visited-set window -- the blocks a compact-window kernel would hand to an overflow pass (the
-round-2 experiment, commit 0a3ee45).
+visited-set window -- the blocks the compact-set kernel hands to its overflow passes
+(DESIGN.md §7 "Compact visited set").
 
   python tools/excursion.py [--configs c3,c4] [--variant 0] [--out f.json]
 
