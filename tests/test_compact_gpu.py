@@ -175,3 +175,32 @@ def test_host_path_chunks_share_the_overflow_list():
     np.testing.assert_array_equal(hsad.numpy().astype(np.uint32), dev[1])
     np.testing.assert_array_equal(hpts.numpy().astype(np.uint16), dev[2])
     np.testing.assert_array_equal(hst.numpy().astype(np.uint64), dev[3])
+
+
+def test_cuda_graph_capture_and_replay():
+    """the compact path (memset, main kernel, two overflow passes) captured into a CUDA graph
+    on torch's capture stream and replayed: outputs equal the eager call's"""
+    os.environ.pop("ME_COMPACT", None)
+    W, H = 320, 256
+    tex = synth.texture(W, H, (6.0, 12.0), 777).numpy()
+    host = np.stack([np.stack(synth.translated_pair(tex, dx, dy)) for dx, dy in [(30, 2), (-3, 1), (5, -28)]])
+    frames = torch.from_numpy(host).to(DEV)
+    eager = _search(frames, 32, 0)
+    assert me.me_dcds_overflow_count() > 0
+    n, nb = frames.shape[0], (W // 16) * (H // 16)
+    mv, sad, pts, st = me.alloc_outputs(n, nb, DEV)
+    g = torch.cuda.CUDAGraph()
+    try:
+        with torch.cuda.graph(g):
+            me.me_set_stream(torch.cuda.current_stream())
+            me.me_dcds_batch(frames, 16, 32, mv, sad, pts, st)
+    finally:
+        me.me_set_stream(torch.cuda.current_stream())
+    for _ in range(2):
+        mv.zero_(); sad.zero_(); pts.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        got = (mv.cpu().numpy(), sad.cpu().numpy().astype(np.uint32), pts.cpu().numpy().astype(np.uint16),
+               st.cpu().numpy().astype(np.uint64))
+        for a, b in zip(got, eager):
+            np.testing.assert_array_equal(a, b)
