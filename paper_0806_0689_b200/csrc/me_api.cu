@@ -497,13 +497,17 @@ int run_fs(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npair
         const int t = atoi(e);
         if (t >= 64 && t <= 512 && t % 32 == 0) nthr = t;
     }
-    // the 8x8 +-16 build (c3) sweeps each dx column whole (fs_kernel SIDE), 4 warps per CTA
-    // (measured on B200, 32 c3 pairs: 1.375 ms at 128 threads, 1.415 at 256, 1.59 at 352;
-    // the chunked kernel 1.59 at 256; ME_FS_SWEEP=0 selects the chunked kernel)
+    // column-sweep builds (fs_kernel SIDE) for the bench geometries: 8x8 / +-16 (c3) with 4
+    // warps per CTA, 16x16 / +-32 (c4) with 8 (measured on B200, 32 pairs: c3 1.375 ms vs 1.59
+    // chunked, c4 18.38 vs 20.10 ms); ME_FS_SWEEP=0 selects the chunked kernel
     const char* sw = getenv("ME_FS_SWEEP");
-    if (block == 8 && p == 16 && a.pitch == 128 && a.nsplit == 1 && !(sw && atoi(sw) == 0)) {
+    const bool sweep = !(sw && atoi(sw) == 0);
+    if (sweep && block == 8 && p == 16 && a.pitch == 128 && a.nsplit == 1) {
         if (!getenv("ME_FS_THREADS")) nthr = 128;
         me::fs_kernel<8, 33, 128><<<grid, nthr, smem, s>>>(tc, tr, a);
+    } else if (sweep && block == 16 && p == 32 && a.pitch == 160 && !getenv("ME_FS_SPLIT")) {
+        a.nsplit = 1;  // one item per (block, dx): the whole column
+        me::fs_kernel<16, 65, 160><<<grid, nthr, smem, s>>>(tc, tr, a);
     } else if (block == 16) {
         me::fs_kernel<16><<<grid, nthr, smem, s>>>(tc, tr, a);
     } else {
@@ -651,6 +655,7 @@ int me_init(int device) {
     if ((rc = allow_smem(me::fs_kernel<16>))) return rc;
     if ((rc = allow_smem(me::fs_kernel<8>))) return rc;
     if ((rc = allow_smem(me::fs_kernel<8, 33, 128>))) return rc;
+    if ((rc = allow_smem(me::fs_kernel<16, 65, 160>))) return rc;
     if (!g_scratch) CK(cudaMalloc(&g_scratch, 64));
     {  // visited-bitmap templates for every p (dcds_kernel.cuh, bm_template_word)
         static uint32_t tmpl[me::BM_TMPL_WORDS];
