@@ -214,7 +214,8 @@ int64_t me_launch_count(void);
  * 16x16 blocks at p >= 26, or as ME_COMPACT forces); 0 when that call did not use the compact
  * set.  Diagnostic only -- the outputs are the same either way.  *count_out is a HOST
  * pointer; waits for that call's overflow passes, then reads the two list counts (interior and
- * border blocks) from the device. */
+ * border blocks) from the device.  A call captured into a CUDA graph writes the counts when
+ * the graph is replayed; synchronise the replay before asking. */
 int me_dcds_overflow_count(uint64_t* count_out);
 
 /* Static description of the last error (never NULL). */

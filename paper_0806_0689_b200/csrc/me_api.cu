@@ -309,17 +309,18 @@ int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npa
     const bool compact_ok = !trace && (long long)npairs * (W / block) * (H / block) < (1ll << 31);
     DcdsLaunch L = plan_dcds(W, H, block, p, npairs, compact_ok);
     if ((int)L.smem > g_smem_optin) return fail(ME_EINVAL, "tile does not fit in shared memory");
+    // a call captured into a CUDA graph neither waits for nor records the ordering event (its
+    // replays are ordered by the caller; an event recorded during capture cannot be waited on)
+    bool capturing = false;
     if (L.a.compact) {
         L.a.ovf_cap = (uint32_t)((long long)npairs * L.a.nb);
         int rc = grow(&g_ovf, &g_ovf_cap, 4 * (4 + (size_t)L.a.ovf_cap));
         if (rc) return rc;
         L.a.ovf = reinterpret_cast<uint32_t*>(g_ovf);
-        if (g_ovf_stream && g_ovf_stream != s) {
-            // (not while s is being captured into a graph: its replays are ordered by the user)
-            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-            CK(cudaStreamIsCapturing(s, &cs));
-            if (cs == cudaStreamCaptureStatusNone) CK(cudaStreamWaitEvent(s, g_ovf_ev, 0));
-        }
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CK(cudaStreamIsCapturing(s, &cs));
+        capturing = cs != cudaStreamCaptureStatusNone;
+        if (!capturing && g_ovf_stream && g_ovf_stream != s) CK(cudaStreamWaitEvent(s, g_ovf_ev, 0));
         CK(cudaMemsetAsync(g_ovf, 0, 16, s));
     }
     g_ovf_used = L.a.compact != 0;
@@ -358,8 +359,10 @@ int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npa
                 me::dcds_redo_kernel<16, 8, 0, false><<<bg, 32, bs_, s>>>(L.a);
             }
             CK(cudaGetLastError());
-            CK(cudaEventRecord(g_ovf_ev, s));
-            g_ovf_stream = s;
+            if (!capturing) {
+                CK(cudaEventRecord(g_ovf_ev, s));
+                g_ovf_stream = s;
+            }
         }
     } else {
         if (variant) launch_dcds_b<8, 1>(L, tc, tr, s); else launch_dcds_b<8, 0>(L, tc, tr, s);

@@ -204,3 +204,17 @@ def test_cuda_graph_capture_and_replay():
                st.cpu().numpy().astype(np.uint64))
         for a, b in zip(got, eager):
             np.testing.assert_array_equal(a, b)
+    # eager calls on another stream after the capture (the capture recorded no ordering event)
+    side = torch.cuda.Stream()
+    me.me_set_stream(side)
+    try:
+        with torch.cuda.stream(side):
+            again = _search(frames, 32, 0)
+    finally:
+        me.me_set_stream(torch.cuda.current_stream())
+    for a, b in zip(again, eager):
+        np.testing.assert_array_equal(a, b)
+    assert me.me_dcds_overflow_count() > 0
+    again = _search(frames, 32, 0)
+    for a, b in zip(again, eager):
+        np.testing.assert_array_equal(a, b)
