@@ -80,6 +80,10 @@ struct SearchArgs {
     int compact;
     uint32_t* ovf;
     uint32_t ovf_cap;  // npairs * nb
+    // warm-start records of the first rec_cap interior entries: the abandoned search's state
+    // (centre, kind, SAD, points) and its compact bitmap, [rec_cap][2 + bm_words]
+    uint32_t* rec;
+    int rec_cap;
 };
 
 __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
@@ -832,8 +836,24 @@ __global__ void __launch_bounds__(NWARP * 32, ONE ? (B == 8 ? 36 / NWARP : (CPT 
             for (int o2 = 1; o2 < G; o2 <<= 1) ss += __shfl_xor_sync(FULL, ss, o2);
             if (live && j == 0) output(ss);
             if (CPT_OK && have && !live && j == 0) {
-                if (redo_interior(a, gblk)) a.ovf[4 + atomicAdd(&a.ovf[0], 1u)] = (uint32_t)gblk;
-                else a.ovf[4 + a.ovf_cap - 1 - atomicAdd(&a.ovf[1], 1u)] = (uint32_t)gblk;
+                // hand the abandoned search to the overflow passes: interior blocks to the
+                // front of the list with a warm-start record (centre, kind, SAD, points, the
+                // compact bitmap) while records last, border blocks to the back
+                if (redo_interior(a, gblk)) {
+                    const uint32_t e = atomicAdd(&a.ovf[0], 1u);
+                    a.ovf[4 + e] = (uint32_t)gblk;
+                    if (e < (uint32_t)a.rec_cap) {
+                        uint32_t* rc = a.rec + (size_t)e * (2 + a.bm_words);
+#pragma unroll 1
+                        for (int w = 0; w < a.bm_words; w++) rc[2 + w] = bm[w * BST];
+                        int cx, cy;
+                        gs.centre(bmx, bmy, cx, cy);
+                        rc[0] = (uint32_t)(cx & 0xff) | ((uint32_t)(cy & 0xff) << 8) | ((uint32_t)gs.kind << 16);
+                        rc[1] = gs.best | ((uint32_t)gs.pts << 16);
+                    }
+                } else {
+                    a.ovf[4 + a.ovf_cap - 1 - atomicAdd(&a.ovf[1], 1u)] = (uint32_t)gblk;
+                }
             }
         }
     } else for (;;) {
@@ -1016,6 +1036,35 @@ __global__ void __launch_bounds__(GLOBAL ? 128 : 32, GLOBAL ? 8 : 1) dcds_redo_k
             gs.init_search(j, bm, 1, bm_init, words, p, p, true);
         } else {
             gs.st = ST_IDLE; gs.want = 0;
+        }
+        if constexpr (GLOBAL) {
+            // warm start: continue the abandoned search from its record -- its compact visited
+            // bits remapped into the full bitmap, its Step-3 state restored (Step 1 is skipped)
+            __syncwarp();  // the group's template words are written before the remap ORs in
+            if (have && e < (uint32_t)a.rec_cap) {
+                const uint32_t* rc = a.rec + (size_t)e * (2 + a.bm_words);
+                const int bwc = 2 * a.bmx + 3, bwf = bm_row(p);
+                for (int w = j; w < a.bm_words; w += G) {
+                    uint32_t v = rc[2 + w];
+                    while (v) {
+                        const int ci = 32 * w + __ffs(v) - 1;
+                        v &= v - 1;
+                        const int row = ci / bwc, dx = ci - row * bwc - (a.bmx + 2), dy = row - (a.bmy + 2);
+                        const int fi = (dy + p + 2) * bwf + (dx + p + 2);
+                        atomicOr(&bm[fi >> 5], 1u << (fi & 31));
+                    }
+                }
+                const uint32_t s0 = rc[0], s1 = rc[1];
+                const int cx = (int)(int8_t)(s0 & 0xff), cy = (int)(int8_t)((s0 >> 8) & 0xff);
+                gs.kind = (int)((s0 >> 16) & 1u);
+                gs.best = s1 & 0xffffu;
+                gs.pts = (int)(s1 >> 16);
+                gs.cidx = (cy + p + 2) * bwf + (cx + p + 2);
+                gs.cpos = gs.bofs + cy * rp + cx;
+                gs.st = ST_S3;
+                gs.want = 0xf;
+                gs.set_ddsp(gs.kind, rp, bwf);
+            }
         }
         __syncwarp();  // the staged windows and bitmaps are visible to the group
         gs.step1(s, j, p, bm_row(p), rp, rstride, jrow);

@@ -34,6 +34,8 @@ int g_sms = 148;
 // overflow list of the compact visited set (SearchArgs::ovf; grow-only, 4 bytes per block)
 uint8_t* g_ovf = nullptr;
 size_t g_ovf_cap = 0;
+uint8_t* g_rec = nullptr;  // warm-start records of the overflow pass (grow-only)
+size_t g_rec_cap = 0;
 bool g_ovf_used = false;  // the last DCDS batch call used the compact set
 // the list is one buffer: a compact call on another stream than the previous one waits for it
 cudaEvent_t g_ovf_ev = nullptr;
@@ -187,6 +189,8 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs, bool allow_compact 
     a.bmx = a.bmy = p;
     a.compact = 0;
     a.ovf = nullptr;
+    a.rec = nullptr;
+    a.rec_cap = 0;
     L.smem = layout(a.bm_words);
     // Compact visited set (B=16 ONE kernels): at +-32 the bitmaps (145 words per
     // group) hold the CTA to 4 per SM; a 51 x 45 window (bmx 24, bmy 20: 72 words) fits 5, and
@@ -317,6 +321,12 @@ int run_dcds(const uint8_t* cur0, const uint8_t* ref0, long long stride, int npa
         int rc = grow(&g_ovf, &g_ovf_cap, 4 * (4 + (size_t)L.a.ovf_cap));
         if (rc) return rc;
         L.a.ovf = reinterpret_cast<uint32_t*>(g_ovf);
+        // warm-start records for the first 1/32 of the blocks (at least 64k) that reach the
+        // interior overflow pass; later ones restart there from the window origin
+        L.a.rec_cap = (int)std::min<long long>(L.a.ovf_cap, std::max<long long>(1 << 16, L.a.ovf_cap / 32));
+        if (const char* e = getenv("ME_REC_CAP")) L.a.rec_cap = std::max(0, std::min(L.a.rec_cap, atoi(e)));  // tests
+        if ((rc = grow(&g_rec, &g_rec_cap, 4 * (size_t)L.a.rec_cap * (2 + L.a.bm_words)))) return rc;
+        L.a.rec = reinterpret_cast<uint32_t*>(g_rec);
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         CK(cudaStreamIsCapturing(s, &cs));
         capturing = cs != cudaStreamCaptureStatusNone;
@@ -966,6 +976,9 @@ void me_shutdown(void) {
     if (g_ovf) cudaFree(g_ovf);
     g_ovf = nullptr;
     g_ovf_cap = 0;
+    if (g_rec) cudaFree(g_rec);
+    g_rec = nullptr;
+    g_rec_cap = 0;
     g_ovf_used = false;
     if (g_ovf_ev) cudaEventDestroy(g_ovf_ev);
     g_ovf_ev = nullptr;

@@ -109,6 +109,34 @@ def test_forced_window_tiny_frames(monkeypatch):
         _check_oracle(host, 7, 0, got)
 
 
+# (window or None = default, p, ME_REC_CAP or None = default)
+WARM = [(None, 32, None), (None, 32, 3), (None, 32, 0), ((6, 4), 12, None), ((5, 3), 16, 5), ((4, 2), 7, None)]
+
+
+@pytest.mark.parametrize("win,p,cap", WARM, ids=[f"w{c[0]}-p{c[1]}-cap{c[2]}" for c in WARM])
+@pytest.mark.parametrize("variant", [0, 1], ids=["dcds", "dcds_s"])
+def test_warm_start_parity(monkeypatch, win, p, cap, variant):
+    """abandoned interior searches continue in the overflow pass from their warm-start records
+    (ME_REC_CAP: only the first few get one, the rest restart from the window origin): every
+    output is still the oracle's"""
+    if win is None:
+        monkeypatch.delenv("ME_COMPACT", raising=False)
+    else:
+        monkeypatch.setenv("ME_COMPACT", f"{win[0]},{win[1]}")
+    if cap is None:
+        monkeypatch.delenv("ME_REC_CAP", raising=False)
+    else:
+        monkeypatch.setenv("ME_REC_CAP", str(cap))
+    W, H = 320, 256
+    kinds = ["far", "texture", "noise", "far", "binary", "flat"]
+    host = np.stack([np.stack(_content(k, W, H, 7 * p + i)) for i, k in enumerate(kinds)])
+    frames = torch.from_numpy(host).to(DEV)
+    got = _search(frames, p, variant)
+    nov = me.me_dcds_overflow_count()
+    _check_oracle(host, p, variant, got)
+    assert nov > 0, "nothing reached the overflow passes"
+
+
 def test_invalid_forced_window_falls_back_to_full(monkeypatch):
     """an out-of-range ME_COMPACT window is ignored (full bitmap): no overflow list in use"""
     monkeypatch.setenv("ME_COMPACT", "3,2")  # bmx < 4
