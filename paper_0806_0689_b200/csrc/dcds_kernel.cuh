@@ -70,7 +70,6 @@ struct SearchArgs {
     uint64_t* trace;            // TRACE builds: [npairs][nb][tcap] pass records
     uint16_t* tlen;             // TRACE builds: [npairs][nb] passes of each block
     int tcap;
-    int pf;                     // L2 prefetch distance in CTAs (0: none)
     // visited-bitmap geometry (half-widths; = p unless compact) and the compact visited set of
     // the B=16 ONE kernels (DESIGN.md §7 "Compact visited set"): a search whose centre leaves
     // the compact window is abandoned and its block index (pair * nb + block) appended to ovf:
@@ -136,12 +135,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
         : "memory");
 }
 
-// L2 prefetch of a 3-D tensor-map box (no shared-memory destination, no completion).
-__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int x, int y, int z) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                     reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z)
-                 : "memory");
-}
 
 // Edge replication (reading C9) of a TMA-staged region whose box reached outside the frame
 // (TMA zero-fills there).  Region rows i <-> frame row ys+i, columns c <-> frame column xs+c.
@@ -154,6 +147,7 @@ __device__ __forceinline__ void fixup_edges(uint8_t* sref, int pitch, int rh, in
     if (cl > 0 || cr < pitch) {
         // xs, W and pitch are multiples of 16: the out-of-frame column spans are whole uint4s
         const int nl = cl >> 4, nr = (pitch - cr) >> 4;
+#pragma unroll 1
         for (int e = threadIdx.x; e < (i1 - i0) * (nl + nr); e += blockDim.x) {
             const int i = i0 + e / (nl + nr), q = e % (nl + nr);
             uint8_t* row = sref + i * pitch;
@@ -164,6 +158,7 @@ __device__ __forceinline__ void fixup_edges(uint8_t* sref, int pitch, int rh, in
     __syncthreads();
     if (i0 > 0 || i1 < rh) {
         const int n16 = pitch >> 4;
+#pragma unroll 1
         for (int e = threadIdx.x; e < rh * n16; e += blockDim.x) {
             const int i = e / n16, q = e - i * n16;
             if (i >= i0 && i < i1) continue;
@@ -736,19 +731,6 @@ __global__ void __launch_bounds__(NWARP * 32, ONE ? (B == 8 ? 36 / NWARP : (CPT 
         tma_load_3d(sref, &tm_ref, xs, ys, pair, bar);
         tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
         *ctr = 0;
-        if (a.pf) {
-            // warm L2 with the tile of the CTA about one resident wave later (CTAs are
-            // scheduled in linear order), so its staging waits on L2 instead of HBM
-            const long long lin = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z) + a.pf;
-            const long long per = (long long)gridDim.x * gridDim.y;
-            if (lin < per * gridDim.z) {
-                const int fz = (int)(lin / per), fr = (int)(lin - (long long)fz * per);
-                const int fy = fr / gridDim.x, fx = fr - fy * gridDim.x;
-                const int fx0 = fx * TW, fy0 = fy * TH;
-                tma_prefetch_3d(&tm_ref, (fx0 - a.p) & ~15, fy0 - a.p, fz);
-                tma_prefetch_3d(&tm_cur, fx0, fy0, fz);
-            }
-        }
     }
     const int bw = 2 * bmx + 3;
     // bitmap templates (border only / border + HCSP), precomputed in constant memory; the

@@ -218,10 +218,6 @@ DcdsLaunch plan_dcds(int W, int H, int B, int p, int npairs, bool allow_compact 
         L.smem = layout(a.bm_words);
     }
     if (const char* e = getenv("ME_SMEM_PAD")) L.smem += (size_t)std::max(0, atoi(e));  // tuning only
-    // L2 prefetch of the tile one resident wave ahead (ME_PF = distance in CTAs; tuning only):
-    // measured slower on B200 (c3 1.442 -> 1.457 ms, c4 16.81 -> 18.79 ms at one wave), so off
-    a.pf = 0;
-    if (const char* e = getenv("ME_PF")) a.pf = std::max(0, atoi(e));
     return L;
 }
 
