@@ -168,13 +168,13 @@ __global__ void __launch_bounds__(NWARP * 32)
     uint32_t* s_code = reinterpret_cast<uint32_t*>(s_off + NROW);
     uint64_t* bar = reinterpret_cast<uint64_t*>(s_code + NROW + (NROW & 1));
 
-    if (threadIdx.x == 0) mbar_init(bar, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // init and issue at once: the barrier publishes the init meanwhile
+        mbar_init(bar, 1);
         mbar_expect_tx(bar, (uint32_t)(pitch * a.rh + TW * TH));
         tma_load_3d(sref, &tm_ref, xs, ys, pair, bar);
         tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
     }
+    __syncthreads();
     for (int r = threadIdx.x; r < NROW; r += NWARP * 32) {
         const uint32_t w = a.rcode[r];
         s_code[r] = w;

@@ -724,14 +724,18 @@ __global__ void __launch_bounds__(NWARP * 32, ONE ? (B == 8 ? 36 / NWARP : (CPT 
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((a.init_off + 8 * a.bm_words + 4 + 7) & ~7));
 
     // ---- stage the tile with TMA: reference region + current tile, one mbarrier
-    if (threadIdx.x == 0) mbar_init(bar, 1);
-    __syncthreads();
     if (threadIdx.x == 0) {
+        // the thread that initialises the mbarrier issues the loads right away (the init is
+        // made visible to the async proxy first); the barrier below publishes the init to the
+        // other threads while the loads are in flight (measured: c4 15.19 -> 14.78 ms against
+        // issuing after the barrier)
+        mbar_init(bar, 1);  // (with fence.mbarrier_init)
         mbar_expect_tx(bar, (uint32_t)(pitch * a.rh + TW * TH));
         tma_load_3d(sref, &tm_ref, xs, ys, pair, bar);
         tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
         *ctr = 0;
     }
+    __syncthreads();
     const int bw = 2 * bmx + 3;
     // bitmap templates (border only / border + HCSP), precomputed in constant memory; the
     // compact set has no border (no bits / the 7 HCSP bits)

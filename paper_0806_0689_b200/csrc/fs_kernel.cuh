@@ -66,14 +66,14 @@ __global__ void __launch_bounds__(512)
     const int tbx_e = min(a.tbx, a.nbx - tx * a.tbx), tby_e = min(a.tby, nby - ty * a.tby);
     const int nbt = tbx_e * tby_e;
 
-    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
-    if (threadIdx.x < 64) s_key[threadIdx.x] = 0xffffffffu;
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // init and issue at once: the barrier publishes the init meanwhile
+        mbar_init(&s_bar, 1);
         mbar_expect_tx(&s_bar, (uint32_t)(pitch * a.rh + TW * TH));
         tma_load_3d(sref, &tm_ref, xs, ys, pair, &s_bar);
         tma_load_3d(scur, &tm_cur, x0, y0, pair, &s_bar);
     }
+    if (threadIdx.x < 64) s_key[threadIdx.x] = 0xffffffffu;
+    __syncthreads();
     mbar_wait(&s_bar, 0);
     if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
         fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
@@ -365,13 +365,13 @@ __global__ void __launch_bounds__(256)
     uint8_t* scur = smem + a.cur_off;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ((a.cur_off + TW * TH + 7) & ~7));
     __shared__ unsigned long long ssum[8];
-    if (threadIdx.x == 0) mbar_init(bar, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // init and issue at once: the barrier publishes the init meanwhile
+        mbar_init(bar, 1);
         mbar_expect_tx(bar, (uint32_t)(pitch * a.rh + TW * TH));
         tma_load_3d(sref, &tm_ref, xs, ys, pair, bar);
         tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
     }
+    __syncthreads();
     mbar_wait(bar, 0);
     if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
         fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
