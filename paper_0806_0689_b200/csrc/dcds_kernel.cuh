@@ -706,11 +706,16 @@ __global__ void __launch_bounds__(NWARP * 32, ONE ? (B == 8 ? 36 / NWARP : (CPT 
     // compact visited set: the B=16 ONE kernels (4-8x8 tiles at +-32 need 5 CTAs/SM)
     constexpr bool CPT_OK = CPT && ONE && B == 16 && !TRACE;
     const bool cpt = CPT_OK && a.compact;
+    // GCUR: the 8x8 ONE kernels load each group's current rows from global memory during the
+    // region's TMA load and initialise the bitmaps before waiting for it (c3 1.407 -> 1.401 ms;
+    // for 16x16 blocks the TMA-staged current tile measured faster: 14.78 vs 15.16 ms at c4)
+    constexpr bool GCUR = ONE && B == 8;
     const int bmx = CPT_OK ? a.bmx : p, bmy = CPT_OK ? a.bmy : p;
 
     // shared layout: reference region (pitch x rh) | current tile (TW x TH) | group bitmaps |
-    // bitmap template | tile counter | mbarrier | per-warp statistics sums (NWARP x 3 u64).  ONE kernels overlay the bitmaps on the current tile,
-    // which is read into registers before the bitmaps are initialised.
+    // bitmap template | tile counter | mbarrier | per-warp statistics sums (NWARP x 3 u64).  ONE
+    // kernels overlay the bitmaps on the current tile (read into registers first; GCUR kernels
+    // read the current rows from global memory and use the space for the bitmaps only).
     uint8_t* sref = smem;
     uint8_t* scur = smem + a.cur_off;
     uint32_t* bms = reinterpret_cast<uint32_t*>(smem + a.bm_off);
@@ -729,10 +734,11 @@ __global__ void __launch_bounds__(NWARP * 32, ONE ? (B == 8 ? 36 / NWARP : (CPT 
         // made visible to the async proxy first); the barrier below publishes the init to the
         // other threads while the loads are in flight (measured: c4 15.19 -> 14.78 ms against
         // issuing after the barrier)
+        // (GCUR kernels read their current rows from global memory: only the region is staged)
         mbar_init(bar, 1);  // (with fence.mbarrier_init)
-        mbar_expect_tx(bar, (uint32_t)(pitch * a.rh + TW * TH));
+        mbar_expect_tx(bar, (uint32_t)(pitch * a.rh + (GCUR ? 0 : TW * TH)));
         tma_load_3d(sref, &tm_ref, xs, ys, pair, bar);
-        tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
+        if (!GCUR) tma_load_3d(scur, &tm_cur, x0, y0, pair, bar);
         *ctr = 0;
     }
     __syncthreads();
@@ -754,10 +760,12 @@ __global__ void __launch_bounds__(NWARP * 32, ONE ? (B == 8 ? 36 / NWARP : (CPT 
             bm_init[t] = c_bm_tmpl[bm_tmpl_off(p) + a.bm_words + t];
         }
     }
-    mbar_wait(bar, 0);
-    if (xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H)
-        fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
-    __syncthreads();
+    const bool border = xs < 0 || ys < 0 || xs + pitch > a.W || ys + a.rh > a.H;
+    if constexpr (!GCUR) {
+        mbar_wait(bar, 0);
+        if (border) fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
+        __syncthreads();
+    }
 
     const uint32_t* s = reinterpret_cast<const uint32_t*>(sref);
     const int rstride = G * pitch;  // bytes between a lane's rows
@@ -776,7 +784,11 @@ __global__ void __launch_bounds__(NWARP * 32, ONE ? (B == 8 ? 36 / NWARP : (CPT 
         const int bxg = x0 + lbx * B, byg = y0 + lby * B;
         gblk = (long long)pair * a.nb + (byg / B) * a.nbx + (bxg / B);
         if (TRACE) { gs.tr = a.trace + gblk * a.tcap; gs.tcap = a.tcap; gs.npass = 0; }
-        gs.load_cur((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW, j);
+        if constexpr (GCUR)  // the current block's rows straight from the frame (L2 / HBM)
+            gs.load_cur((byg - ys) * pitch + (bxg - xs), a.cur0 + (long long)pair * a.stride + (long long)byg * a.W + bxg,
+                        a.W, j);
+        else
+            gs.load_cur((byg - ys) * pitch + (bxg - xs), scur + (lby * B) * TW + lbx * B, TW, j);
 #ifdef ME_DEBUG
         gs.dbg_region = pitch * a.rh;
         gs.dbg_bits = 32 * a.bm_words;
@@ -795,14 +807,19 @@ __global__ void __launch_bounds__(NWARP * 32, ONE ? (B == 8 ? 36 / NWARP : (CPT 
     if constexpr (ONE) {
         const int idx = warp * NG + g;
         const bool have = idx < nbt;
-        if (have) take(idx);
-        __syncthreads();  // every current row is in registers: the bitmaps may overwrite them
-        // all bitmaps of the CTA at once: word w of every group, dense 16-byte stores
+        if (have) take(idx);  // (GCUR: global loads, in flight with the region's TMA load)
+        __syncthreads();  // the templates are written; every current row is in registers
+        // all bitmaps of the CTA at once: word w of every group, dense 16-byte stores (over the
+        // current tile, which is in registers by now)
         for (int e = threadIdx.x; e < a.bm_words * (BST / 4); e += NWARP * 32) {
             const uint32_t v = bm_init[e / (BST / 4)];  // constant divisor
             reinterpret_cast<uint4*>(bms)[e] = make_uint4(v, v, v, v);
         }
-        __syncthreads();
+        if constexpr (GCUR) {
+            mbar_wait(bar, 0);
+            if (border) fixup_edges(sref, pitch, a.rh, xs, ys, a.W, a.H);
+        }
+        __syncthreads();  // the bitmaps (and an edge-fixed region) are visible
         if (have) gs.init_search(j, bm, BST, bm_init, a.bm_words, bmx, bmy, false);
         else { gs.st = ST_IDLE; gs.want = 0; }
         if (__any_sync(FULL, have)) {
